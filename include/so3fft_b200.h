@@ -1,0 +1,139 @@
+/*
+ * so3fft_b200 -- C ABI of the B200-native FSOFT / iFSOFT (Kostelec-Rockmore SO(3) FFT).
+ *
+ * Drop-in boundary for the reference Python package `so3fft` (arXiv 1808.00896,
+ * /root/reference/pkg/src/so3fft).  The reference has no FFI of its own: its
+ * operator interface is the Python surface re-exported by __init__.py:17-94.
+ * Each entry point below names the reference function it replaces (file:line,
+ * relative to pkg/src/so3fft).  The Python mirror
+ * `paper_1808_00896_b200` binds these with ctypes.
+ *
+ * Data: complex128 as interleaved (re, im) float64 pairs, little endian.
+ *   samples      : (2B)^3 per function, C order over [i = alpha][j = beta][k = gamma]
+ *                  (core.py:148-176, So3SampleGrid)
+ *   coefficients : B(4B^2-1)/3 per function, l-major, slot(l,m,m') =
+ *                  l(4l^2-1)/3 + (m+l)(2l+1) + (m'+l)   (core.py:54-61, So3Coefficients)
+ *   batch        : functions are consecutive (stride (2B)^3 resp. B(4B^2-1)/3).
+ * Pointers marked `dev` are CUDA device pointers on the plan's device; `host`
+ * pointers are ordinary host memory.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Every call is asynchronous on `stream` unless noted.
+ *
+ * Errors: every function returns SO3_OK (0) or a nonzero status; the message of
+ * the last failure on the calling thread is so3_last_error().  SO3_ERR_INVALID
+ * corresponds to the reference's ValueError (bad bandwidth, size or argument).
+ */
+#ifndef SO3FFT_B200_H
+#define SO3FFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SO3_OK 0
+#define SO3_ERR_INVALID 1   /* ValueError in the reference */
+#define SO3_ERR_CUDA 2      /* CUDA runtime / launch failure */
+#define SO3_ERR_NOMEM 3     /* device or host allocation failed */
+
+typedef struct so3_plan_s* so3_plan_t;
+
+/* Message of the last failure on this thread ("" if none). */
+const char* so3_last_error(void);
+
+/* Library version string. */
+const char* so3_version(void);
+
+/* ---- host-only helpers (no GPU needed) ------------------------------------ */
+
+/* coeff_count (core.py:48-51): B(4B^2-1)/3; 0 for B < 1. */
+int64_t so3_coeff_count(int bandwidth);
+
+/* grid_size(B)^3 (core.py:43-45): (2B)^3; 0 for B < 1. */
+int64_t so3_grid_count(int bandwidth);
+
+/* coeff_index (core.py:54-61); -1 if (l, m, m') is outside the band. */
+int64_t so3_coeff_index(int l, int m, int mp, int bandwidth);
+
+/* quadrature_weights (quadrature.py:66-73): w_B(j), j < 2B, into host out[2B]. */
+int so3_quadrature_weights(int bandwidth, double* out_host);
+
+/* sample_angles (quadrature.py:57-63): alpha_i (= gamma_i) and beta_j, host out[2B] each. */
+int so3_sample_angles(int bandwidth, double* alphas_host, double* betas_host);
+
+/* Number of symmetry clusters (schedule.py:136-158): 1 + 2(B-1) + (B-1)(B-2)/2. */
+int64_t so3_cluster_count(int bandwidth);
+
+/* The plan's cluster schedule: base pairs (m, m') as int32 pairs in launch order
+ * (longest first), plus their member counts.  bases_host[2*count], members_host[count]
+ * (either may be NULL).  Replaces enumerate_clusters / make_work_items
+ * (schedule.py:136-178) as the unit of GPU work. */
+int so3_cluster_schedule(int bandwidth, int32_t* bases_host, int32_t* members_host);
+
+/* ---- plans ---------------------------------------------------------------- */
+
+/* make_plan (soft.py:80-108) for `batch` functions on the current CUDA device.
+ * Builds the beta tables, quadrature weights, twiddles and the cluster schedule
+ * on the host (long double), uploads them and allocates the plan's scratch
+ * spectrum ((2B)^3 * batch complex128).  matrix_policy / partitioner of the
+ * reference have no effect on results and are handled by the Python layer. */
+int so3_plan_create(int bandwidth, int batch, so3_plan_t* out);
+void so3_plan_destroy(so3_plan_t plan);
+int so3_plan_bandwidth(so3_plan_t plan);
+int so3_plan_batch(so3_plan_t plan);
+int so3_plan_device(so3_plan_t plan);
+/* Device bytes owned by the plan (tables + scratch). */
+int64_t so3_plan_device_bytes(so3_plan_t plan);
+
+/* ---- whole transforms ------------------------------------------------------ */
+
+/* fsoft_sequential / fsoft_parallel (soft.py:124-149, 176-183):
+ * samples_dev (batch x (2B)^3) -> coeffs_dev (batch x C(B)).  Inputs are not modified. */
+int so3_fsoft(so3_plan_t plan, const void* samples_dev, void* coeffs_dev, void* stream);
+
+/* ifsoft_sequential / ifsoft_parallel (soft.py:152-173, 186-193):
+ * coeffs_dev -> samples_dev.  Inputs are not modified. */
+int so3_ifsoft(so3_plan_t plan, const void* coeffs_dev, void* samples_dev, void* stream);
+
+/* Same with HOST buffers: copies in, transforms, copies out, and synchronises
+ * `stream` before returning (the reference API's numpy-in / numpy-out contract).
+ * Device staging buffers are allocated on first use and kept by the plan. */
+int so3_fsoft_host(so3_plan_t plan, const void* samples_host, void* coeffs_host, void* stream);
+int so3_ifsoft_host(so3_plan_t plan, const void* coeffs_host, void* samples_host, void* stream);
+
+/* ---- stages (parity tests, per-stage timing, sharded pipeline) ------------ */
+
+/* Forward torus stage: for every beta slice the sign +1 2-D DFT
+ * (fft.py:72-76 via soft.py:130-132) times the quadrature weight w_j, written
+ * pair-major: spectrum_dev[f][m mod 2B][m' mod 2B][j] (column m' = B unwritten). */
+int so3_fft_analysis(so3_plan_t plan, const void* samples_dev, void* spectrum_dev, void* stream);
+
+/* Inverse torus stage: sign -1 2-D DFT per slice (soft.py:164-172) of
+ * spectrum_dev[f][m][m'][j] (rows/columns at the Nyquist bin B read as zero).
+ * spectrum_dev is used as scratch (overwritten). */
+int so3_fft_synthesis(so3_plan_t plan, void* spectrum_dev, void* samples_dev, void* stream);
+
+/* Forward DWT (dwt.py:109-116 per member, soft.py:134-148) over clusters
+ * [cluster_begin, cluster_end) of the schedule; reads the weighted spectrum written
+ * by so3_fft_analysis and writes those clusters' coefficient slots. */
+int so3_dwt_analysis(so3_plan_t plan, const void* spectrum_dev, void* coeffs_dev,
+                     int64_t cluster_begin, int64_t cluster_end, void* stream);
+
+/* Inverse DWT (dwt.py:119-125 per member, soft.py:157-167) over clusters
+ * [cluster_begin, cluster_end): writes spectrum_dev[f][m][m'][j] of their pairs. */
+int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_dev,
+                      int64_t cluster_begin, int64_t cluster_end, void* stream);
+
+/* Scratch spectrum owned by the plan (device pointer, batch x (2B)^3 complex128). */
+void* so3_plan_scratch(so3_plan_t plan);
+
+/* Wigner rows d^l_{m,m'}(beta_j), l = max(|m|,|m'|)..B-1, j < 2B, for any pair
+ * (wigner_d_rows, wigner.py:139-178 + derive_cluster_matrices, dwt.py:76-93):
+ * out_dev[(l-L)*2B + j], generated by the same in-register recurrence as the DWT. */
+int so3_wigner_rows(so3_plan_t plan, int m, int mp, double* out_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SO3FFT_B200_H */

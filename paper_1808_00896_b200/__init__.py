@@ -1,0 +1,52 @@
+"""B200-native FSOFT / iFSOFT -- drop-in for the hot path of the reference `so3fft`.
+
+Public names follow the reference's export table (pkg/src/so3fft/__init__.py:17-94)
+for the transform path: containers and layouts (core), grid/weights, clusters,
+make_plan / fsoft_* / ifsoft_*.  Compute runs in libso3fft_b200.so (hand-written
+sm_100a CUDA, include/so3fft_b200.h); there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+from .core import (
+    FORMAT_VERSION,
+    SOFC_MAGIC,
+    SOFG_MAGIC,
+    So3Coefficients,
+    So3SampleGrid,
+    coeff_count,
+    coeff_index,
+    degree_of_slots,
+    grid_size,
+    order_pair_slots,
+    read_coefficients,
+    read_samples,
+    validate_bandwidth,
+    write_coefficients,
+    write_samples,
+)
+from .soft import (
+    OrderPair,
+    QuadratureWeights,
+    SampleAngles,
+    SymmetryCluster,
+    TransformPlan,
+    cluster_for_base,
+    cluster_schedule,
+    dwt_analysis,
+    dwt_synthesis,
+    fft_analysis,
+    fft_synthesis,
+    fsoft_batch,
+    fsoft_parallel,
+    fsoft_sequential,
+    ifsoft_batch,
+    ifsoft_parallel,
+    ifsoft_sequential,
+    make_plan,
+    quadrature_weights,
+    sample_angles,
+    wigner_rows,
+)
+
+__version__ = "0.1.0"

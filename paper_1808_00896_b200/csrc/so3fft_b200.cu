@@ -1,0 +1,488 @@
+// so3fft_b200: plan construction (host, long double) and the C ABI of include/so3fft_b200.h.
+//
+// Reference mapping (pkg/src/so3fft):
+//   make_plan          soft.py:80-108     -> so3_plan_create
+//   _fsoft             soft.py:124-149    -> so3_fsoft  = fft_analysis + dwt_analysis
+//   _ifsoft            soft.py:152-173    -> so3_ifsoft = dwt_synthesis + fft_synthesis
+//   quadrature_weights quadrature.py:66-73, sample_angles quadrature.py:57-63
+//   enumerate_clusters schedule.py:136-158 (kappa order) -> cost-sorted launch order
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/so3fft_b200.h"
+#include "common.cuh"
+#include "dwt.cuh"
+#include "fft.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+#define SO3_CUDA(call)                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = (call);                                                                   \
+    if (_e != cudaSuccess)                                                                     \
+      return fail(SO3_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+bool valid_bandwidth(int b) { return b >= 1 && b <= 4096; }
+
+// ---------------------------------------------------------------- host tables
+
+const long double kPi = 3.141592653589793238462643383279502884L;
+
+void host_weights(int b, double* out) {
+  // w_B(j) = (2 pi / B^2) sin(beta_j) sum_{i<B} sin((2i+1) beta_j) / (2i+1)  (quadrature.py:66-73)
+  const int n = 2 * b;
+  for (int j = 0; j < n; ++j) {
+    const long double beta = (2.0L * j + 1.0L) * kPi / (4.0L * b);
+    long double s = 0.0L;
+    for (int i = 0; i < b; ++i) s += sinl((2.0L * i + 1.0L) * beta) / (2.0L * i + 1.0L);
+    out[j] = (double)((2.0L * kPi / ((long double)b * b)) * sinl(beta) * s);
+  }
+}
+
+struct Cluster { int m, mp, members; };
+
+// Symmetry clusters of base pairs 0 <= m' <= m < B (schedule.py:123-158), ordered by
+// cost = members * (B - m) descending so the hardware CTA scheduler runs the longest
+// first (the GPU form of the reference's dynamic schedule, schedule.py:228-242).
+std::vector<Cluster> host_clusters(int b) {
+  std::vector<Cluster> cl;
+  cl.reserve((size_t)b * (b + 1) / 2);
+  for (int m = 0; m < b; ++m)
+    for (int mp = 0; mp <= m; ++mp) {
+      const int mem = (m == 0) ? 1 : (mp == 0 || mp == m) ? 4 : 8;
+      cl.push_back({m, mp, mem});
+    }
+  std::stable_sort(cl.begin(), cl.end(), [b](const Cluster& x, const Cluster& y) {
+    const long long cx = (long long)x.members * (b - x.m), cy = (long long)y.members * (b - y.m);
+    if (cx != cy) return cx > cy;
+    if (x.m != y.m) return x.m < y.m;
+    return x.mp < y.mp;
+  });
+  return cl;
+}
+
+void split_ld(long double v, double* hi, double* lo) {
+  *hi = (double)v;
+  *lo = (double)(v - (long double)*hi);
+}
+
+}  // namespace
+
+struct so3_plan_s {
+  int B = 0, n = 0, batch = 1, device = 0;
+  int64_t ncoef = 0, ngrid = 0, nclusters = 0;
+  int2* d_bases = nullptr;
+  double2* d_lnorm = nullptr;
+  double* d_cosb = nullptr;
+  double4* d_logcs = nullptr;
+  double* d_w = nullptr;
+  double2* d_tw = nullptr;
+  double2* d_scratch = nullptr;
+  // staging for the host-buffer entry points
+  double2* d_grid_stage = nullptr;
+  double2* d_coef_stage = nullptr;
+  int64_t bytes = 0;
+};
+
+// ------------------------------------------------------------------ launches
+
+namespace {
+
+template <int N, int JB>
+int launch_fft_pow2(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
+  const int threads = JB * N / 16;
+  const size_t smem = (size_t)JB * (N + 1) * sizeof(double2);
+  dim3 grid((a.J + JB - 1) / JB, a.n, batch);
+  void (*k)(so3::FftArgs) = nullptr;
+  if (mode == so3::ROW_FWD) k = so3::fft_pass_kernel<N, JB, +1, so3::ROW_FWD>;
+  else if (mode == so3::ROW_INV) k = so3::fft_pass_kernel<N, JB, -1, so3::ROW_INV>;
+  else if (sign > 0) k = so3::fft_pass_kernel<N, JB, +1, so3::COL>;
+  else k = so3::fft_pass_kernel<N, JB, -1, so3::COL>;
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, threads, smem, st>>>(a);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int launch_fft_direct(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
+  const int JC = std::max(1, std::min(a.J, 2048 / a.n));
+  const size_t smem = (size_t)JC * a.n * sizeof(double2);
+  dim3 grid((a.J + JC - 1) / JC, a.n, batch);
+  void (*k)(so3::FftArgs, int) = nullptr;
+  if (mode == so3::ROW_FWD) k = so3::dft_direct_kernel<+1, so3::ROW_FWD>;
+  else if (mode == so3::ROW_INV) k = so3::dft_direct_kernel<-1, so3::ROW_INV>;
+  else if (sign > 0) k = so3::dft_direct_kernel<+1, so3::COL>;
+  else k = so3::dft_direct_kernel<-1, so3::COL>;
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<grid, 256, smem, st>>>(a, JC);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int launch_fft(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
+  switch (a.n) {
+    case 16: return launch_fft_pow2<16, 16>(a, mode, sign, batch, st);
+    case 32: return launch_fft_pow2<32, 32>(a, mode, sign, batch, st);
+    case 64: return launch_fft_pow2<64, 32>(a, mode, sign, batch, st);
+    case 128: return launch_fft_pow2<128, 32>(a, mode, sign, batch, st);
+    case 256: return launch_fft_pow2<256, 16>(a, mode, sign, batch, st);
+    case 512: return launch_fft_pow2<512, 8>(a, mode, sign, batch, st);
+    case 1024: return launch_fft_pow2<1024, 4>(a, mode, sign, batch, st);
+    case 2048: return launch_fft_pow2<2048, 2>(a, mode, sign, batch, st);
+    default: return launch_fft_direct(a, mode, sign, batch, st);
+  }
+}
+
+so3::FftArgs fft_args(const so3_plan_s* p, const void* src, void* dst) {
+  so3::FftArgs a;
+  a.n = p->n;
+  a.nyq = p->B;
+  a.J = p->n;
+  a.jbase = 0;
+  a.src = static_cast<const double2*>(src);
+  a.dst = static_cast<double2*>(dst);
+  a.tw = p->d_tw;
+  a.w = p->d_w;
+  a.fstride_src = p->ngrid;
+  a.fstride_dst = p->ngrid;
+  return a;
+}
+
+int dwt_jt(int n) {
+  // threads per cluster = ceil(n / JT) rounded up to a warp, <= 256
+  if (n >= 128) return std::max(4, (n + 255) / 256);
+  if (n >= 64) return 2;
+  return 1;
+}
+
+template <bool ANALYSIS>
+int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st) {
+  if (c0 < 0 || c1 > p->nclusters || c0 > c1)
+    return fail(SO3_ERR_INVALID, "cluster range [" + std::to_string(c0) + ", " + std::to_string(c1) +
+                                     ") outside [0, " + std::to_string(p->nclusters) + ")");
+  if (c0 == c1) return SO3_OK;
+  so3::DwtArgs a;
+  a.B = p->B;
+  a.n = p->n;
+  a.bases = p->d_bases;
+  a.lnorm = p->d_lnorm;
+  a.cosb = p->d_cosb;
+  a.logcs = p->d_logcs;
+  a.spec = static_cast<const double2*>(spec);
+  a.coef = static_cast<double2*>(coef);
+  a.spec_fstride = p->ngrid;
+  a.coef_fstride = p->ncoef;
+  a.cluster0 = (int)c0;
+  const int jt = dwt_jt(p->n);
+  const int threads = std::min(256, ((p->n + jt - 1) / jt + 31) / 32 * 32);
+  dim3 grid((unsigned)(c1 - c0), p->batch);
+  switch (jt) {
+    case 1: if (ANALYSIS) so3::dwt_analysis_kernel<1><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<1><<<grid, threads, 0, st>>>(a); break;
+    case 2: if (ANALYSIS) so3::dwt_analysis_kernel<2><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<2><<<grid, threads, 0, st>>>(a); break;
+    case 4: if (ANALYSIS) so3::dwt_analysis_kernel<4><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<4><<<grid, threads, 0, st>>>(a); break;
+    case 8: if (ANALYSIS) so3::dwt_analysis_kernel<8><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<8><<<grid, threads, 0, st>>>(a); break;
+    default: return fail(SO3_ERR_INVALID, "bandwidth too large for the DWT kernels (JT > 8)");
+  }
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+// Rows of d^l_{m,m'} for any pair: base recurrence + relation (sign, reflection).
+__global__ void wigner_rows_kernel(int B, int n, int m, int mp, int bm, int bmp, int reflect, int sl, int par0,
+                                   double2 lnorm, const double* cosb, const double4* logcs, double* out) {
+  const int L = bm;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double x = cosb[j];
+    double cur = so3::seed_value(bm, bmp, lnorm, logcs[j]);
+    double prev = 0.0;
+    const int jo = reflect ? n - 1 - j : j;
+    for (int l = L; l < B; ++l) {
+      const double s = ((sl * l + par0) & 1) ? -1.0 : 1.0;
+      out[(long long)(l - L) * n + jo] = s * cur;
+      if (l < B - 1) {
+        const double3 k3 = so3::recurrence_coeffs(l, bm, bmp);
+        const double tt = fma(k3.x, x, -k3.y);
+        const double nx = fma(tt, cur, -k3.z * prev);
+        prev = cur;
+        cur = nx;
+      }
+    }
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* so3_last_error(void) { return g_last_error.c_str(); }
+const char* so3_version(void) { return "so3fft_b200 0.1.0 (sm_100a, fp64)"; }
+
+int64_t so3_coeff_count(int b) { return b < 1 ? 0 : (int64_t)b * (4LL * b * b - 1) / 3; }
+int64_t so3_grid_count(int b) { return b < 1 ? 0 : (int64_t)(2LL * b) * (2LL * b) * (2LL * b); }
+
+int64_t so3_coeff_index(int l, int m, int mp, int b) {
+  if (b < 1 || l < 0 || l >= b || std::abs(m) > l || std::abs(mp) > l) return -1;
+  const int64_t L = l;
+  return L * (4 * L * L - 1) / 3 + (int64_t)(m + l) * (2 * l + 1) + (mp + l);
+}
+
+int so3_quadrature_weights(int b, double* out) {
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  if (!out) return fail(SO3_ERR_INVALID, "null output");
+  host_weights(b, out);
+  return SO3_OK;
+}
+
+int so3_sample_angles(int b, double* alphas, double* betas) {
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  for (int i = 0; i < 2 * b; ++i) {
+    if (alphas) alphas[i] = (double)i * 3.141592653589793 / (double)b;          // quadrature.py:60
+    if (betas) betas[i] = (2.0 * i + 1.0) * 3.141592653589793 / (4.0 * b);     // quadrature.py:61
+  }
+  return SO3_OK;
+}
+
+int64_t so3_cluster_count(int b) { return b < 1 ? 0 : (int64_t)b * (b + 1) / 2; }
+
+int so3_cluster_schedule(int b, int32_t* bases, int32_t* members) {
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  const auto cl = host_clusters(b);
+  for (size_t i = 0; i < cl.size(); ++i) {
+    if (bases) { bases[2 * i] = cl[i].m; bases[2 * i + 1] = cl[i].mp; }
+    if (members) members[i] = cl[i].members;
+  }
+  return SO3_OK;
+}
+
+int so3_plan_create(int b, int batch, so3_plan_t* out) {
+  if (!out) return fail(SO3_ERR_INVALID, "null plan output");
+  *out = nullptr;
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  if (batch < 1) return fail(SO3_ERR_INVALID, "batch must be >= 1, got " + std::to_string(batch));
+  if (b > 1024) return fail(SO3_ERR_INVALID, "bandwidth > 1024 does not fit one device");
+  auto* p = new so3_plan_s();
+  p->B = b;
+  p->n = 2 * b;
+  p->batch = batch;
+  p->ncoef = so3_coeff_count(b);
+  p->ngrid = so3_grid_count(b);
+  cudaGetDevice(&p->device);
+  const int n = p->n;
+
+  std::vector<double> w(n), cosb(n);
+  std::vector<double4> logcs(n);
+  std::vector<double2> tw(n);
+  host_weights(b, w.data());
+  for (int j = 0; j < n; ++j) {
+    const long double beta = (2.0L * j + 1.0L) * kPi / (4.0L * b);
+    cosb[j] = (double)cosl(beta);
+    double a0, a1, a2, a3;
+    split_ld(logl(cosl(0.5L * beta)), &a0, &a1);
+    split_ld(logl(sinl(0.5L * beta)), &a2, &a3);
+    logcs[j] = make_double4(a0, a1, a2, a3);
+  }
+  for (int k = 0; k < n; ++k) {
+    const long double th = 2.0L * kPi * k / n;
+    tw[k] = make_double2((double)cosl(th), (double)sinl(th));
+  }
+  const auto cl = host_clusters(b);
+  p->nclusters = (int64_t)cl.size();
+  std::vector<int2> bases(cl.size());
+  std::vector<double2> lnorm(cl.size());
+  for (size_t i = 0; i < cl.size(); ++i) {
+    const int m = cl[i].m, mp = cl[i].mp;
+    bases[i] = make_int2(m, mp);
+    // log sqrt((2m)! / ((m+m')! (m-m')!))   (wigner.py:124)
+    const long double ln = 0.5L * (lgammal(2.0L * m + 1) - lgammal((long double)m + mp + 1) - lgammal((long double)m - mp + 1));
+    double hi, lo;
+    split_ld(ln, &hi, &lo);
+    lnorm[i] = make_double2(hi, lo);
+  }
+
+  auto cleanup = [p]() { so3_plan_destroy(p); };
+#define PLAN_ALLOC(ptr, count)                                                                    \
+  do {                                                                                            \
+    size_t _bytes = (size_t)(count) * sizeof(*(ptr));                                             \
+    cudaError_t _e = cudaMalloc((void**)&(ptr), _bytes);                                          \
+    if (_e != cudaSuccess) { cleanup(); return fail(SO3_ERR_NOMEM, std::string("cudaMalloc(") +  \
+                                 std::to_string(_bytes) + "): " + cudaGetErrorString(_e)); }      \
+    p->bytes += (int64_t)_bytes;                                                                  \
+  } while (0)
+  PLAN_ALLOC(p->d_bases, cl.size());
+  PLAN_ALLOC(p->d_lnorm, cl.size());
+  PLAN_ALLOC(p->d_cosb, n);
+  PLAN_ALLOC(p->d_logcs, n);
+  PLAN_ALLOC(p->d_w, n);
+  PLAN_ALLOC(p->d_tw, n);
+  PLAN_ALLOC(p->d_scratch, (size_t)p->ngrid * batch);
+#undef PLAN_ALLOC
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMemcpy(p->d_bases, bases.data(), bases.size() * sizeof(int2), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_lnorm, lnorm.data(), lnorm.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_cosb, cosb.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_logcs, logcs.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cleanup(); return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e)); }
+  *out = p;
+  return SO3_OK;
+}
+
+void so3_plan_destroy(so3_plan_t p) {
+  if (!p) return;
+  cudaFree(p->d_bases);
+  cudaFree(p->d_lnorm);
+  cudaFree(p->d_cosb);
+  cudaFree(p->d_logcs);
+  cudaFree(p->d_w);
+  cudaFree(p->d_tw);
+  cudaFree(p->d_scratch);
+  cudaFree(p->d_grid_stage);
+  cudaFree(p->d_coef_stage);
+  delete p;
+}
+
+int so3_plan_bandwidth(so3_plan_t p) { return p ? p->B : 0; }
+int so3_plan_batch(so3_plan_t p) { return p ? p->batch : 0; }
+int so3_plan_device(so3_plan_t p) { return p ? p->device : -1; }
+int64_t so3_plan_device_bytes(so3_plan_t p) { return p ? p->bytes : 0; }
+void* so3_plan_scratch(so3_plan_t p) { return p ? p->d_scratch : nullptr; }
+
+#define CHECK_PLAN(p) \
+  if (!(p)) return fail(SO3_ERR_INVALID, "null plan")
+#define CHECK_PTR(x) \
+  if (!(x)) return fail(SO3_ERR_INVALID, "null buffer: " #x)
+
+int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
+  if (samples == spectrum) return fail(SO3_ERR_INVALID, "fft_analysis cannot run in place");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  so3::FftArgs a = fft_args(p, samples, spectrum);
+  int rc = launch_fft(a, so3::ROW_FWD, +1, p->batch, st);      // K1a: gamma axis, transposing write
+  if (rc) return rc;
+  a = fft_args(p, spectrum, spectrum);
+  return launch_fft(a, so3::COL, +1, p->batch, st);            // K1b: alpha axis * w_j, in place
+}
+
+int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
+  if (samples == spectrum) return fail(SO3_ERR_INVALID, "fft_synthesis cannot run in place");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  so3::FftArgs a = fft_args(p, spectrum, spectrum);
+  int rc = launch_fft(a, so3::COL, -1, p->batch, st);          // K4a: m -> alpha, in place
+  if (rc) return rc;
+  a = fft_args(p, spectrum, samples);
+  return launch_fft(a, so3::ROW_INV, -1, p->batch, st);        // K4b: m' -> gamma, transposing read
+}
+
+int so3_dwt_analysis(so3_plan_t p, const void* spectrum, void* coeffs, int64_t c0, int64_t c1, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(spectrum); CHECK_PTR(coeffs);
+  return launch_dwt<true>(p, spectrum, coeffs, c0, c1, static_cast<cudaStream_t>(stream));
+}
+
+int so3_dwt_synthesis(so3_plan_t p, const void* coeffs, void* spectrum, int64_t c0, int64_t c1, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(spectrum); CHECK_PTR(coeffs);
+  // the synthesis kernel writes the spectrum; DwtArgs carries it as `spec` and reads `coef`
+  return launch_dwt<false>(p, spectrum, const_cast<void*>(coeffs), c0, c1, static_cast<cudaStream_t>(stream));
+}
+
+int so3_fsoft(so3_plan_t p, const void* samples, void* coeffs, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(coeffs);
+  int rc = so3_fft_analysis(p, samples, p->d_scratch, stream);
+  if (rc) return rc;
+  return so3_dwt_analysis(p, p->d_scratch, coeffs, 0, p->nclusters, stream);
+}
+
+int so3_ifsoft(so3_plan_t p, const void* coeffs, void* samples, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(coeffs);
+  int rc = so3_dwt_synthesis(p, coeffs, p->d_scratch, 0, p->nclusters, stream);
+  if (rc) return rc;
+  return so3_fft_synthesis(p, p->d_scratch, samples, stream);
+}
+
+static int ensure_stage(so3_plan_t p) {
+  if (!p->d_grid_stage) {
+    cudaError_t e = cudaMalloc((void**)&p->d_grid_stage, (size_t)p->ngrid * p->batch * sizeof(double2));
+    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("staging grid: ") + cudaGetErrorString(e));
+    p->bytes += p->ngrid * p->batch * (int64_t)sizeof(double2);
+  }
+  if (!p->d_coef_stage) {
+    cudaError_t e = cudaMalloc((void**)&p->d_coef_stage, (size_t)p->ncoef * p->batch * sizeof(double2));
+    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("staging coefficients: ") + cudaGetErrorString(e));
+    p->bytes += p->ncoef * p->batch * (int64_t)sizeof(double2);
+  }
+  return SO3_OK;
+}
+
+int so3_fsoft_host(so3_plan_t p, const void* samples_host, void* coeffs_host, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples_host); CHECK_PTR(coeffs_host);
+  int rc = ensure_stage(p);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SO3_CUDA(cudaMemcpyAsync(p->d_grid_stage, samples_host, (size_t)p->ngrid * p->batch * sizeof(double2),
+                           cudaMemcpyHostToDevice, st));
+  rc = so3_fsoft(p, p->d_grid_stage, p->d_coef_stage, stream);
+  if (rc) return rc;
+  SO3_CUDA(cudaMemcpyAsync(coeffs_host, p->d_coef_stage, (size_t)p->ncoef * p->batch * sizeof(double2),
+                           cudaMemcpyDeviceToHost, st));
+  SO3_CUDA(cudaStreamSynchronize(st));
+  return SO3_OK;
+}
+
+int so3_ifsoft_host(so3_plan_t p, const void* coeffs_host, void* samples_host, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(samples_host); CHECK_PTR(coeffs_host);
+  int rc = ensure_stage(p);
+  if (rc) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SO3_CUDA(cudaMemcpyAsync(p->d_coef_stage, coeffs_host, (size_t)p->ncoef * p->batch * sizeof(double2),
+                           cudaMemcpyHostToDevice, st));
+  rc = so3_ifsoft(p, p->d_coef_stage, p->d_grid_stage, stream);
+  if (rc) return rc;
+  SO3_CUDA(cudaMemcpyAsync(samples_host, p->d_grid_stage, (size_t)p->ngrid * p->batch * sizeof(double2),
+                           cudaMemcpyDeviceToHost, st));
+  SO3_CUDA(cudaStreamSynchronize(st));
+  return SO3_OK;
+}
+
+int so3_wigner_rows(so3_plan_t p, int m, int mp, double* out, void* stream) {
+  CHECK_PLAN(p); CHECK_PTR(out);
+  const int L = std::max(std::abs(m), std::abs(mp));
+  if (L >= p->B) return fail(SO3_ERR_INVALID, "order pair has no degrees below B");
+  // find the base pair 0 <= b' <= b and the relation mapping it to (m, m')
+  static const int rel[8][8] = {{0, 0, 0, 0, 1, 0, 0, 1},  {0, 0, 1, 1, -1, 0, 0, -1}, {0, 0, 1, 1, 0, 1, 1, 0},
+                                {0, 0, 0, 0, 0, -1, -1, 0}, {1, 1, 0, 1, -1, 0, 0, 1},  {1, 1, 1, 0, 1, 0, 0, -1},
+                                {1, 1, 0, 1, 0, -1, 1, 0},  {1, 1, 1, 0, 0, 1, -1, 0}};
+  const int bm = std::max(std::abs(m), std::abs(mp)), bmp = std::min(std::abs(m), std::abs(mp));
+  int tag = -1;
+  for (int k = 0; k < 8 && tag < 0; ++k) {
+    const int tm = rel[k][4] * bm + rel[k][5] * bmp, tp = rel[k][6] * bm + rel[k][7] * bmp;
+    if (tm == m && tp == mp) tag = k;
+  }
+  if (tag < 0) return fail(SO3_ERR_INVALID, "no symmetry relation reaches the pair");
+  const long double ln = 0.5L * (lgammal(2.0L * bm + 1) - lgammal((long double)bm + bmp + 1) - lgammal((long double)bm - bmp + 1));
+  double hi, lo;
+  split_ld(ln, &hi, &lo);
+  const int par0 = (rel[tag][2] * bm + rel[tag][3] * bmp) & 1;
+  wigner_rows_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      p->B, p->n, m, mp, bm, bmp, rel[tag][0], rel[tag][1], par0, make_double2(hi, lo), p->d_cosb, p->d_logcs, out);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,393 @@
+"""Drop-in FSOFT / iFSOFT on B200: plans and transforms (mirrors reference soft.py).
+
+Reference surface kept (pkg/src/so3fft/soft.py):
+    make_plan(bandwidth, matrix_policy="streaming", partitioner="kappa")   soft.py:80-108
+    fsoft_sequential(samples, plan) / fsoft_parallel(samples, plan, threads) soft.py:176-183
+    ifsoft_sequential(coeffs, plan) / ifsoft_parallel(coeffs, plan, threads) soft.py:186-193
+Every transform runs the CUDA path of libso3fft_b200.so (include/so3fft_b200.h);
+there is no CPU path.  ``threads`` is validated like the reference
+(schedule.py:216-217) and otherwise has no effect: results are identical for
+every value, which is the reference's own guarantee (soft.py:7-10).
+
+Input/output types follow the input: numpy in -> numpy out (host buffers,
+copied in and out by the library, the reference's contract); torch complex128
+CUDA tensors in -> torch tensors out on the same device, on the current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from typing import Any, NamedTuple
+
+import numpy as np
+
+from . import _native
+from .core import (
+    So3Coefficients,
+    So3SampleGrid,
+    _is_torch,
+    coeff_count,
+    degree_scale,
+    grid_size,
+    order_pair_slots,
+    validate_bandwidth,
+)
+
+_MATRIX_POLICIES = ("streaming", "precomputed")
+_PARTITIONERS = ("kappa", "sigma")
+
+
+class OrderPair(NamedTuple):
+    m: int
+    mp: int
+
+
+# relation tags per cluster kind, reference schedule.py:115-120
+_TAGS = {
+    "origin": ("identity",),
+    "axis": ("identity", "negate_both", "swap", "swap_negate_both"),
+    "diagonal": ("identity", "negate_both", "negate_m", "negate_mp"),
+    "full": ("identity", "negate_both", "swap", "swap_negate_both",
+             "negate_m", "negate_mp", "swap_negate_m", "swap_negate_mp"),
+}
+# target map (tm_m, tm_mp, tp_m, tp_mp) per tag, reference wigner.py:244-256
+_TARGET = {
+    "identity": (1, 0, 0, 1), "negate_both": (-1, 0, 0, -1), "swap": (0, 1, 1, 0),
+    "swap_negate_both": (0, -1, -1, 0), "negate_m": (-1, 0, 0, 1), "negate_mp": (1, 0, 0, -1),
+    "swap_negate_m": (0, -1, 1, 0), "swap_negate_mp": (0, 1, -1, 0),
+}
+
+
+class SymmetryCluster(NamedTuple):
+    """Base pair and its orbit (reference schedule.py:93-103); members are (pair, tag)."""
+    kind: str
+    base: OrderPair
+    members: tuple
+
+
+def cluster_for_base(m: int, mp: int) -> SymmetryCluster:
+    """reference schedule.py:123-133."""
+    if not 0 <= mp <= m:
+        raise ValueError(f"base pair must satisfy 0 <= m' <= m, got ({m}, {mp})")
+    kind = "origin" if m == 0 else "axis" if mp == 0 else "diagonal" if mp == m else "full"
+    members = []
+    for tag in _TAGS[kind]:
+        a, b, c, d = _TARGET[tag]
+        members.append((OrderPair(a * m + b * mp, c * m + d * mp), tag))
+    return SymmetryCluster(kind, OrderPair(m, mp), tuple(members))
+
+
+@dataclass(frozen=True, eq=False)
+class SampleAngles:
+    """Per-axis angles of the grid (reference quadrature.py:26-39)."""
+    bandwidth: int
+    alphas: np.ndarray = field(repr=False)
+    betas: np.ndarray = field(repr=False)
+    gammas: np.ndarray = field(repr=False)
+
+
+@dataclass(frozen=True, eq=False)
+class QuadratureWeights:
+    """Beta weights w_B(j) (reference quadrature.py:42-54)."""
+    bandwidth: int
+    values: np.ndarray = field(repr=False)
+
+
+def sample_angles(bandwidth: int) -> SampleAngles:
+    """alpha_i = gamma_i = i pi / B, beta_j = (2j+1) pi / (4B) (quadrature.py:57-63), from the C library."""
+    b = validate_bandwidth(bandwidth)
+    al = np.empty(2 * b)
+    be = np.empty(2 * b)
+    _native.check(_native.lib().so3_sample_angles(b, _dptr(al), _dptr(be)), "sample_angles")
+    return SampleAngles(b, al, be, al.copy())
+
+
+def quadrature_weights(bandwidth: int) -> QuadratureWeights:
+    """w_B(j) (quadrature.py:66-73), computed by the C library in long double."""
+    b = validate_bandwidth(bandwidth)
+    w = np.empty(2 * b)
+    _native.check(_native.lib().so3_quadrature_weights(b, _dptr(w)), "quadrature_weights")
+    return QuadratureWeights(b, w)
+
+
+def cluster_schedule(bandwidth: int) -> tuple[np.ndarray, np.ndarray]:
+    """GPU launch order of the symmetry clusters: (bases int32 [K,2], member counts int32 [K])."""
+    b = validate_bandwidth(bandwidth)
+    k = int(_native.lib().so3_cluster_count(b))
+    bases = np.empty((k, 2), dtype=np.int32)
+    mem = np.empty(k, dtype=np.int32)
+    _native.check(_native.lib().so3_cluster_schedule(
+        b, bases.ctypes.data_as(_native._i32p), mem.ctypes.data_as(_native._i32p)), "cluster_schedule")
+    return bases, mem
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_native._dp)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class TransformPlan:
+    """Reusable per-bandwidth GPU state (reference soft.py:56-77).
+
+    Holds the native plan (beta tables, weights, twiddles, cluster schedule,
+    scratch spectrum) on one CUDA device.  ``matrix_policy`` is accepted for API
+    compatibility; Wigner matrices are never stored (they are regenerated in
+    registers by the recurrence), so "precomputed" computes the same values and
+    ``matrices`` is always None.
+    """
+
+    def __init__(self, bandwidth: int, matrix_policy: str, partitioner: str, batch: int, device):
+        torch = _torch()
+        self.bandwidth = bandwidth
+        self.matrix_policy = matrix_policy
+        self.partitioner = partitioner
+        self.batch = batch
+        if not torch.cuda.is_available():
+            raise RuntimeError("so3fft_b200 needs a CUDA device (there is no CPU path)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        self.matrices = None
+        self.angles = sample_angles(bandwidth)
+        self.weights = quadrature_weights(bandwidth)
+        self.degree_scale = degree_scale(bandwidth)
+        self._clusters = None
+        self._slot_table = None
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            torch.empty(1, device=self.device)   # make the primary context current
+            _native.check(_native.lib().so3_plan_create(bandwidth, batch, ctypes.byref(handle)), "make_plan")
+        self._handle = handle
+        self.n_clusters = int(_native.lib().so3_cluster_count(bandwidth))
+
+    # -- reference attributes, built lazily (O(B^2) Python objects / O(B^3) ints)
+    @property
+    def clusters(self) -> list[SymmetryCluster]:
+        if self._clusters is None:
+            b = self.bandwidth
+            if self.partitioner == "kappa":       # schedule.py:146-153
+                bases = [(0, 0)] + [(m, 0) for m in range(1, b)] + [(m, m) for m in range(1, b)]
+                for kappa in range((b - 1) * (b - 2) // 2):
+                    i, j = kappa // (b - 1) + 1, kappa % (b - 1) + 1
+                    bases.append((b - i, b - j) if j > i else (i + 1, j))
+            else:                                  # schedule.py:154-157
+                bases = []
+                for s in range(b * (b + 1) // 2):
+                    m = int(math.floor(math.sqrt(2.0 * s + 0.25) - 0.5))
+                    bases.append((m, s - m * (m + 1) // 2))
+            self._clusters = [cluster_for_base(m, mp) for m, mp in bases]
+        return self._clusters
+
+    @property
+    def work_items(self) -> list[tuple[int, SymmetryCluster]]:
+        return list(enumerate(self.clusters))
+
+    @property
+    def slot_table(self) -> dict:
+        if self._slot_table is None:
+            self._slot_table = {pair: order_pair_slots(pair.m, pair.mp, self.bandwidth)
+                                for c in self.clusters for pair, _ in c.members}
+        return self._slot_table
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if self._handle is None:
+            raise ValueError("plan has been released")
+        return self._handle
+
+    @property
+    def device_bytes(self) -> int:
+        return int(_native.lib().so3_plan_device_bytes(self.handle))
+
+    def release(self) -> None:
+        if getattr(self, "_handle", None) is not None:
+            _native.lib().so3_plan_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.release()
+        except Exception:
+            pass
+
+    def __repr__(self) -> str:
+        return (f"TransformPlan(bandwidth={self.bandwidth}, batch={self.batch}, device={self.device}, "
+                f"matrix_policy={self.matrix_policy!r}, partitioner={self.partitioner!r})")
+
+
+def make_plan(bandwidth: int, matrix_policy: str = "streaming", partitioner: str = "kappa", *,
+              batch: int = 1, device=None) -> TransformPlan:
+    """Build the reusable plan for one bandwidth (reference soft.py:80-108).
+
+    Extensions: ``batch`` functions per call (configs' B=32 x 64 case) and
+    ``device`` (default: the current CUDA device).
+    """
+    b = validate_bandwidth(bandwidth)
+    if matrix_policy not in _MATRIX_POLICIES:
+        raise ValueError(f"matrix_policy must be one of {_MATRIX_POLICIES}, got {matrix_policy!r}")
+    if partitioner not in _PARTITIONERS:
+        raise ValueError(f"unknown partitioner {partitioner!r}")
+    if isinstance(batch, bool) or not isinstance(batch, (int, np.integer)) or batch < 1:
+        raise ValueError(f"batch must be an integer >= 1, got {batch!r}")
+    return TransformPlan(b, matrix_policy, partitioner, int(batch), device)
+
+
+def _check_plan(data_bandwidth: int, plan: TransformPlan, what: str) -> int:
+    """reference soft.py:118-121."""
+    if data_bandwidth != plan.bandwidth:
+        raise ValueError(f"{what} bandwidth {data_bandwidth} does not match plan bandwidth {plan.bandwidth}")
+    return plan.bandwidth
+
+
+def _check_threads(threads) -> None:
+    """reference schedule.py:216-217."""
+    if isinstance(threads, bool) or not isinstance(threads, (int, np.integer)) or threads < 1:
+        raise ValueError(f"threads must be an integer >= 1, got {threads!r}")
+
+
+def _stream(plan: TransformPlan):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
+
+
+def _run(plan: TransformPlan, data, out_count: int, dev_fn: str, host_fn: str, out=None):
+    """Dispatch a whole transform on device tensors or host arrays (batch-aware)."""
+    torch = _torch()
+    lib = _native.lib()
+    total = out_count * plan.batch
+    if _is_torch(data):
+        if not data.is_cuda:
+            data = data.to(plan.device)
+        if data.device != plan.device:
+            raise ValueError(f"data on {data.device}, plan on {plan.device}")
+        data = data.contiguous()
+        if data.dtype != torch.complex128:
+            raise ValueError("device data must be complex128")
+        if out is None:
+            out = torch.empty(total, dtype=torch.complex128, device=plan.device)
+        with torch.cuda.device(plan.device):
+            _native.check(getattr(lib, dev_fn)(plan.handle, ctypes.c_void_p(data.data_ptr()),
+                                               ctypes.c_void_p(out.data_ptr()), _stream(plan)), dev_fn)
+        return out
+    arr = np.ascontiguousarray(data, dtype=np.complex128)
+    if out is None:
+        out = np.empty(total, dtype=np.complex128)
+    with torch.cuda.device(plan.device):
+        _native.check(getattr(lib, host_fn)(plan.handle, ctypes.c_void_p(arr.ctypes.data),
+                                            ctypes.c_void_p(out.ctypes.data), _stream(plan)), host_fn)
+    return out
+
+
+def _fsoft(samples: So3SampleGrid, plan: TransformPlan, out=None) -> So3Coefficients:
+    b = _check_plan(samples.bandwidth, plan, "sample")
+    if plan.batch != 1:
+        raise ValueError(f"plan is for batch={plan.batch}; use fsoft_batch")
+    n = grid_size(b)
+    data = samples.data
+    if (data.shape[0] if hasattr(data, "shape") else len(data)) != n ** 3:
+        raise ValueError(f"sample data must have length {n ** 3}")
+    res = _run(plan, data, coeff_count(b), "so3_fsoft", "so3_fsoft_host", out)
+    return So3Coefficients(b, res)
+
+
+def _ifsoft(coeffs: So3Coefficients, plan: TransformPlan, out=None) -> So3SampleGrid:
+    b = _check_plan(coeffs.bandwidth, plan, "coefficient")
+    if plan.batch != 1:
+        raise ValueError(f"plan is for batch={plan.batch}; use ifsoft_batch")
+    data = coeffs.data
+    if (data.shape[0] if hasattr(data, "shape") else len(data)) != coeff_count(b):
+        raise ValueError(f"coefficient data must have length {coeff_count(b)}")
+    res = _run(plan, data, grid_size(b) ** 3, "so3_ifsoft", "so3_ifsoft_host", out)
+    return So3SampleGrid(b, res)
+
+
+def fsoft_sequential(samples: So3SampleGrid, plan: TransformPlan, *, out=None) -> So3Coefficients:
+    """Forward transform (reference soft.py:176-178)."""
+    return _fsoft(samples, plan, out)
+
+
+def fsoft_parallel(samples: So3SampleGrid, plan: TransformPlan, threads: int, *, out=None) -> So3Coefficients:
+    """Forward transform; identical values for every ``threads`` (reference soft.py:181-183)."""
+    _check_threads(threads)
+    return _fsoft(samples, plan, out)
+
+
+def ifsoft_sequential(coeffs: So3Coefficients, plan: TransformPlan, *, out=None) -> So3SampleGrid:
+    """Inverse transform (reference soft.py:186-188)."""
+    return _ifsoft(coeffs, plan, out)
+
+
+def ifsoft_parallel(coeffs: So3Coefficients, plan: TransformPlan, threads: int, *, out=None) -> So3SampleGrid:
+    """Inverse transform; identical values for every ``threads`` (reference soft.py:191-193)."""
+    _check_threads(threads)
+    return _ifsoft(coeffs, plan, out)
+
+
+def fsoft_batch(samples, plan: TransformPlan, *, out=None):
+    """Forward transform of plan.batch functions: samples (batch, (2B)^3) -> (batch, C(B))."""
+    b = plan.bandwidth
+    flat = samples.reshape(-1)
+    if flat.shape[0] != plan.batch * grid_size(b) ** 3:
+        raise ValueError(f"expected {plan.batch} x {grid_size(b) ** 3} samples")
+    res = _run(plan, flat, coeff_count(b), "so3_fsoft", "so3_fsoft_host", out)
+    return res.reshape(plan.batch, coeff_count(b))
+
+
+def ifsoft_batch(coeffs, plan: TransformPlan, *, out=None):
+    """Inverse transform of plan.batch functions: (batch, C(B)) -> (batch, (2B)^3)."""
+    b = plan.bandwidth
+    flat = coeffs.reshape(-1)
+    if flat.shape[0] != plan.batch * coeff_count(b):
+        raise ValueError(f"expected {plan.batch} x {coeff_count(b)} coefficients")
+    res = _run(plan, flat, grid_size(b) ** 3, "so3_ifsoft", "so3_ifsoft_host", out)
+    return res.reshape(plan.batch, grid_size(b) ** 3)
+
+
+# ------------------------------------------------------------------ stages (device tensors only)
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def fft_analysis(plan: TransformPlan, samples, spectrum) -> None:
+    """K1: weighted torus spectrum spectrum[f][m][m'][j] of device samples (fft.py:72-76, soft.py:130-132)."""
+    _native.check(_native.lib().so3_fft_analysis(plan.handle, _ptr(samples), _ptr(spectrum), _stream(plan)),
+                  "fft_analysis")
+
+
+def fft_synthesis(plan: TransformPlan, spectrum, samples) -> None:
+    """K4: samples from spectrum[f][m][m'][j] (soft.py:164-172); spectrum is overwritten."""
+    _native.check(_native.lib().so3_fft_synthesis(plan.handle, _ptr(spectrum), _ptr(samples), _stream(plan)),
+                  "fft_synthesis")
+
+
+def dwt_analysis(plan: TransformPlan, spectrum, coeffs, begin: int = 0, end: int | None = None) -> None:
+    """K2: forward DWT of clusters [begin, end) of the launch schedule (dwt.py:109-116)."""
+    end = plan.n_clusters if end is None else end
+    _native.check(_native.lib().so3_dwt_analysis(plan.handle, _ptr(spectrum), _ptr(coeffs), begin, end,
+                                                  _stream(plan)), "dwt_analysis")
+
+
+def dwt_synthesis(plan: TransformPlan, coeffs, spectrum, begin: int = 0, end: int | None = None) -> None:
+    """K3: inverse DWT of clusters [begin, end) (dwt.py:119-125)."""
+    end = plan.n_clusters if end is None else end
+    _native.check(_native.lib().so3_dwt_synthesis(plan.handle, _ptr(coeffs), _ptr(spectrum), begin, end,
+                                                   _stream(plan)), "dwt_synthesis")
+
+
+def wigner_rows(plan: TransformPlan, m: int, mp: int):
+    """d^l_{m,m'}(beta_j) for l = L..B-1 on the plan's grid, from the GPU recurrence
+    (wigner_d_rows wigner.py:139-178 + derive_cluster_matrices dwt.py:76-93): (B-L, 2B) float64 tensor."""
+    torch = _torch()
+    b = plan.bandwidth
+    lo = max(abs(m), abs(mp))
+    if lo >= b:
+        raise ValueError(f"order pair (m={m}, m'={mp}) has no degrees below B={b}")
+    out = torch.empty((b - lo, 2 * b), dtype=torch.float64, device=plan.device)
+    _native.check(_native.lib().so3_wigner_rows(plan.handle, m, mp, _ptr(out), _stream(plan)), "wigner_rows")
+    return out
