@@ -1,0 +1,445 @@
+#!/usr/bin/env python3
+"""Benchmark: FSOFT + iFSOFT throughput on B200 (BASELINE.json metric).
+
+One step = one iFSOFT (seeded coefficients -> samples) followed by one FSOFT
+(samples -> coefficients) of one function at bandwidth B, the reference
+benchmark protocol (pkg/src/so3fft/bench.py:146-209).  Each step is two
+transforms; ``value`` = transforms/s of the whole job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--bandwidth B]
+  python bench.py --impl reference ...     # CPU reference arm (oracle port, all host cores)
+
+Rank 0 prints ONE JSON line.  Under torchrun (N > 1) each rank runs an
+independent replica of the single-GPU step ("Multi-GPU");
+the timed region is bracketed by a barrier + synchronize and the max over
+ranks is reported.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")   # reference bench.py:21-24: pin BLAS before numpy loads
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_B = 512
+
+
+def coeff_count(b: int) -> int:
+    return b * (4 * b * b - 1) // 3
+
+
+def seeded_coefficients(b: int, seed: int) -> np.ndarray:
+    """BASELINE.json configs: real and imaginary parts i.i.d. N(0,1), default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    c = coeff_count(b)
+    return rng.standard_normal(c) + 1j * rng.standard_normal(c)
+
+
+def dwt_flops(b: int) -> float:
+    """Algorithmic DWT flops per transform direction: 8 * B * C(B)."""
+    return 8.0 * b * coeff_count(b)
+
+
+def fft_bytes(b: int) -> float:
+    """Algorithmic torus-FFT bytes per direction: read + write (2B)^3 complex128 = 256 B^3."""
+    return 256.0 * b ** 3
+
+
+def measured_peaks() -> dict:
+    peaks = {"fp64_tflops": 36.97, "fp64_source": "measured DMMA m8n8k4 burst, profiles/r01_fp64_peak.log",
+             "hbm_gbs": 6553.3, "hbm_source": "fallback 6553.3 (MEASURED_PEAKS.json absent)"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            mp = json.load(fh)
+        if "hbm_gbs" in mp:
+            peaks["hbm_gbs"] = float(mp["hbm_gbs"])
+            peaks["hbm_source"] = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    fp = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(fp):
+        with open(fp) as fh:
+            peaks.update(json.load(fh))
+    return peaks
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"so3_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as fh:
+            for line in fh:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        load = [s for s in sm if smax and s > 0.5 * max(smax)] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows if r[3].replace(".", "").isdigit())}
+
+
+# --------------------------------------------------------------------------- CPU baseline (oracle port)
+
+_POOL_DATA = None
+
+
+def _slice_job(j):
+    from oracle import so3_oracle as O
+    cube, sign = _POOL_DATA["cube"], _POOL_DATA["sign"]
+    return O.slice_dft(cube[:, j, :], sign)
+
+
+def _cluster_job(i):
+    from oracle import so3_oracle as O
+    fn = O._inverse_cluster if _POOL_DATA["direction"] == "inverse" else O._forward_cluster
+    return fn(_POOL_DATA["jobs"][i])
+
+
+def _timed_pool_map(fn, count: int, workers: int) -> float:
+    """Fork a pool (outside the timed region), time map(fn, range(count)) on it."""
+    import multiprocessing as mp
+    if workers <= 1:
+        t0 = time.perf_counter()
+        for i in range(count):
+            fn(i)
+        return time.perf_counter() - t0
+    with mp.get_context("fork").Pool(processes=workers) as pool:
+        pool.map(abs, range(workers))           # workers are up before the clock starts
+        t0 = time.perf_counter()
+        pool.map(fn, range(count), chunksize=max(1, count // (workers * 4)))
+        return time.perf_counter() - t0
+
+
+def cpu_sample_rate(b: int, seed: int, workers: int, slice_sample: int, cluster_sample: int) -> dict:
+    """Time the oracle (numpy restatement of the reference, oracle/so3_oracle.py) on a bounded
+    random sample of the B workload on a fork pool of `workers` processes (the reference's
+    own parallel scheme, schedule.py:200-248), and extrapolate to whole transforms.
+
+    Per direction: slice DFTs of `slice_sample` random beta slices (x 2B / sample) plus the
+    DWT work items of `cluster_sample` random symmetry clusters (x clusters / sample; the
+    mean of a uniform sample is unbiased for the total).  Pool start-up is not timed.
+    """
+    global _POOL_DATA
+    from oracle import so3_oracle as O
+    n = 2 * b
+    rng = np.random.default_rng(seed)
+    bases = O.base_pairs(b)
+    ks = rng.choice(len(bases), size=min(cluster_sample, len(bases)), replace=False)
+    sample_bases = [bases[k] for k in sorted(ks)]
+    nsl = min(slice_sample, n)
+    cube = rng.standard_normal((n, nsl, n)) + 1j * rng.standard_normal((n, nsl, n))
+    O._plan(b)   # plan tables outside the timed region (reference bench.py:156-158)
+    t = {}
+    for direction, sign in (("inverse", -1), ("forward", +1)):
+        _POOL_DATA = {"cube": cube, "sign": sign}
+        t_fft = _timed_pool_map(_slice_job, nsl, workers) * n / nsl
+        jobs = []
+        for (bm, bmp) in sample_bases:
+            mem = O.cluster_members(bm, bmp)
+            k = b - bm
+            size = k if direction == "inverse" else n
+            jobs.append((b, bm, bmp, [rng.standard_normal(size) + 1j * rng.standard_normal(size) for _ in mem]))
+        _POOL_DATA = {"jobs": jobs, "direction": direction}
+        t_dwt = _timed_pool_map(_cluster_job, len(jobs), workers) * len(bases) / len(jobs)
+        t[direction] = t_fft + t_dwt
+        t[direction + "_fft_s"] = t_fft
+        t[direction + "_dwt_s"] = t_dwt
+    _POOL_DATA = None
+    t["transforms_per_s"] = 2.0 / (t["inverse"] + t["forward"])
+    t["sample"] = (f"B={b}: {nsl}/{n} beta slices and {len(jobs)}/{len(bases)} symmetry clusters per direction "
+                   f"(random, seed {seed}) on a {workers}-process fork pool, extrapolated to whole iFSOFT+FSOFT")
+    return t
+
+
+def run_reference_arm(args, rank: int, world: int) -> None:
+    """--impl reference: the oracle port of the reference path on all host cores, rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import so3_oracle as O
+    b = args.bandwidth
+    workers = O.default_workers()
+    rates, samples = [], None
+    for s in range(args.warmup + args.steps):
+        r = cpu_sample_rate(b, 7000 + s, workers, args.cpu_slices, args.cpu_clusters)
+        if s >= args.warmup:
+            rates.append(r["transforms_per_s"])
+            samples = r["sample"]
+    v = statistics.mean(rates)
+    line = {
+        "impl": "reference", "metric": metric_name(b), "value": v, "unit": "transforms/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 2000.0 / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(b, world),
+        "cpu_baseline": {"value": v, "unit": "transforms/s", "cores": workers, "kind": "port", "sample": samples},
+        "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+
+def metric_name(b: int) -> str:
+    return f"FSOFT+iFSOFT transforms/sec (B={b}, fp64)"
+
+
+def workload_config(b: int, world: int) -> dict:
+    return {"workload": f"BASELINE configs: B={b} single function, complex128, coefficients N(0,1) seed={b}; "
+                        "iFSOFT then FSOFT", "bandwidth": b, "functions_per_step": 1,
+            "grid": f"{2 * b}^3 complex128 ({16 * (2 * b) ** 3 / 1e9:.2f} GB)",
+            "coefficients": coeff_count(b),
+            "l2": "inputs larger than L2 (126 MB)" if 16 * (2 * b) ** 3 > 126e6 else "L2 flushed between steps",
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
+
+
+def l2_flush(torch, buf):
+    buf.add_(1.0)
+
+
+def run_gpu_arm(args, rank: int, world: int, dist) -> None:
+    import torch
+    import paper_1808_00896_b200 as so3
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    b = args.bandwidth
+    n = 2 * b
+    C = coeff_count(b)
+    plan = so3.make_plan(b, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    host_c = seeded_coefficients(b, b)
+    coeffs = torch.from_numpy(host_c).to(dev)
+    grid = torch.empty(n ** 3, dtype=torch.complex128, device=dev)
+    spec = torch.empty(n ** 3, dtype=torch.complex128, device=dev)
+    out = torch.empty(C, dtype=torch.complex128, device=dev)
+    flush = None
+    if 16 * n ** 3 <= 126e6 * 2:
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
+
+    n_ev = 5
+    def step(evs=None):
+        if flush is not None:
+            l2_flush(torch, flush)
+        if evs is not None:
+            evs[0].record(stream)
+        so3.dwt_synthesis(plan, coeffs, spec)          # K3
+        if evs is not None:
+            evs[1].record(stream)
+        so3.fft_synthesis(plan, spec, grid)            # K4a + K4b
+        if evs is not None:
+            evs[2].record(stream)
+        so3.fft_analysis(plan, grid, spec)             # K1a + K1b
+        if evs is not None:
+            evs[3].record(stream)
+        so3.dwt_analysis(plan, spec, out)              # K2
+        if evs is not None:
+            evs[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    time.sleep(0.3 if clocks else 0)
+    # stage-resolved pass (events between stages on the launching stream)
+    stage_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for k in range(args.steps):
+        step(stage_ev[k])
+    t_end.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    ms_total = t_start.elapsed_time(t_end)
+    clk = clocks.stop() if clocks else None
+    stage_names = ["dwt_synthesis", "fft_synthesis", "fft_analysis", "dwt_analysis"]
+    stage_ms = {nm: statistics.mean(stage_ev[k][i].elapsed_time(stage_ev[k][i + 1]) for k in range(args.steps))
+                for i, nm in enumerate(stage_names)}
+    if dist is not None:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * 2.0 * 1000.0 / ms_step
+
+    # parity of the measured output: round trip recovers the seeded coefficients
+    got = out.cpu().numpy()
+    diff = np.abs(got - host_c)
+    rt_abs = float(diff.max())
+    rt_rel = float((diff / np.abs(host_c)).max())
+    rt_rel_max = float(diff.max() / np.abs(host_c).max())
+
+    # end to end through the public API with pinned host buffers (the reference's numpy contract)
+    e2e = None
+    if not args.no_e2e:
+        h_c = torch.empty(C, dtype=torch.complex128, pin_memory=True).numpy()
+        h_c[:] = host_c
+        h_g = torch.empty(n ** 3, dtype=torch.complex128, pin_memory=True).numpy()
+        h_o = torch.empty(C, dtype=torch.complex128, pin_memory=True).numpy()
+        def e2e_step():
+            g = so3.ifsoft_sequential(so3.So3Coefficients(b, h_c), plan, out=h_g)
+            so3.fsoft_sequential(so3.So3SampleGrid(b, g.data), plan, out=h_o)
+        for _ in range(max(1, min(args.warmup, 2))):
+            e2e_step()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ksteps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(ksteps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1) / ksteps
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e_err = float(np.abs(h_o - host_c).max())
+        e2e = {"value": world * 2000.0 / e_ms, "unit": "transforms/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": 16 * (C + n ** 3), "d2h_bytes_per_step": 16 * (n ** 3 + C),
+               "steps": ksteps, "roundtrip_max_abs": e2e_err,
+               "api": "ifsoft_sequential(So3Coefficients numpy, pinned) -> fsoft_sequential(So3SampleGrid numpy)"}
+
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    p64 = peaks["fp64_tflops"] * 1e12
+    bw = peaks["hbm_gbs"] * 1e9
+    fl = dwt_flops(b)
+    by = fft_bytes(b)
+    dom = max(("dwt_analysis", "dwt_synthesis"), key=lambda k: stage_ms[k])
+    achieved = fl / (stage_ms[dom] * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get(f"B{b}", {}).get(dom)
+    roof = {"kernel": f"{dom} (dwt_{'analysis' if dom == 'dwt_analysis' else 'synthesis'}_kernel)",
+            "bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
+            "peak_source": peaks["fp64_source"],
+            "algorithmic": f"8*B*C(B) = {fl:.4g} flop per launch (one transform direction)"}
+    stages = {}
+    for nm in stage_names:
+        ms = stage_ms[nm]
+        if nm.startswith("dwt"):
+            stages[nm] = {"ms": ms, "tflops": fl / (ms * 1e-3) / 1e12, "frac_fp64": fl / (ms * 1e-3) / p64}
+        else:
+            stages[nm] = {"ms": ms, "gbs": by / (ms * 1e-3) / 1e9, "frac_hbm": by / (ms * 1e-3) / bw,
+                          "note": "two HBM passes; algorithmic bytes = one read + one write of the grid"}
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        from oracle import so3_oracle as O
+        r = cpu_sample_rate(b, 4242, O.default_workers(), args.cpu_slices, args.cpu_clusters)
+        cpu = {"value": r["transforms_per_s"], "unit": "transforms/s", "cores": O.default_workers(),
+               "kind": "port", "sample": r["sample"],
+               "est_seconds": {"inverse": r["inverse"], "forward": r["forward"]}}
+    line = {
+        "metric": metric_name(b), "value": value, "unit": "transforms/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(b, world),
+        "fsoft_per_s": world * 1000.0 / (stage_ms["fft_analysis"] + stage_ms["dwt_analysis"]),
+        "ifsoft_per_s": world * 1000.0 / (stage_ms["dwt_synthesis"] + stage_ms["fft_synthesis"]),
+        "stages": stages, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": 6 * args.steps,
+        "clocks": clk,
+        "parity": {"roundtrip_max_abs": rt_abs, "roundtrip_max_rel_per_slot": rt_rel,
+                   "roundtrip_max_rel_of_max": rt_rel_max},
+        "peaks": peaks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--bandwidth", "-B", type=int, default=DEFAULT_B)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-slices", type=int, default=64)
+    ap.add_argument("--cpu-clusters", type=int, default=2048)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the timing rules require >= 3 warm-up steps", file=sys.stderr)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    run_gpu_arm(args, rank, world, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
