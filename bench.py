@@ -254,6 +254,7 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     n = 2 * b
     C = coeff_count(b)
     plan = so3.make_plan(b, device=dev)
+    plan.set_dwt_variant(args.dwt_variant)
     stream = torch.cuda.current_stream(dev)
 
     host_c = seeded_coefficients(b, b)
@@ -415,6 +416,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--bandwidth", "-B", type=int, default=DEFAULT_B)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--dwt-variant", choices=("mma", "simt"), default="mma")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

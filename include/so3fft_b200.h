@@ -125,6 +125,12 @@ int so3_dwt_analysis(so3_plan_t plan, const void* spectrum_dev, void* coeffs_dev
 int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_dev,
                       int64_t cluster_begin, int64_t cluster_end, void* stream);
 
+/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4 contraction) or
+ * SO3_DWT_SIMT (DFMA + warp-butterfly reduction).  Same results to rounding. */
+#define SO3_DWT_MMA 0
+#define SO3_DWT_SIMT 1
+int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
+
 /* Scratch spectrum owned by the plan (device pointer, batch x (2B)^3 complex128). */
 void* so3_plan_scratch(so3_plan_t plan);
 

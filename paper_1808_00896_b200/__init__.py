@@ -35,6 +35,7 @@ from .soft import (
     cluster_schedule,
     dwt_analysis,
     dwt_synthesis,
+    enumerate_clusters,
     fft_analysis,
     fft_synthesis,
     fsoft_batch,

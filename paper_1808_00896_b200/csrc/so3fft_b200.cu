@@ -18,6 +18,7 @@
 #include "../../include/so3fft_b200.h"
 #include "common.cuh"
 #include "dwt.cuh"
+#include "dwt_mma.cuh"
 #include "fft.cuh"
 
 namespace {
@@ -92,10 +93,13 @@ struct so3_plan_s {
   double* d_w = nullptr;
   double2* d_tw = nullptr;
   double2* d_scratch = nullptr;
+  double* d_rc = nullptr;            // recurrence coefficient table
+  long long* d_rc_off = nullptr;
   // staging for the host-buffer entry points
   double2* d_grid_stage = nullptr;
   double2* d_coef_stage = nullptr;
   int64_t bytes = 0;
+  int dwt_variant = SO3_DWT_MMA;
 };
 
 // ------------------------------------------------------------------ launches
@@ -163,10 +167,56 @@ so3::FftArgs fft_args(const so3_plan_s* p, const void* src, void* dst) {
 }
 
 int dwt_jt(int n) {
-  // threads per cluster = ceil(n / JT) rounded up to a warp, <= 256
+  // SIMT kernels: threads per cluster = ceil(n / JT) rounded up to a warp, <= 256
   if (n >= 128) return std::max(4, (n + 255) / 256);
   if (n >= 64) return 2;
   return 1;
+}
+
+int dwt_jw(int n) {
+  // MMA kernels: beta indices per warp (warps per cluster = ceil(n / JW) <= 8)
+  if (n >= 512) return 128;
+  if (n >= 128) return 64;
+  return 32;
+}
+
+template <int JW, int WPC>
+int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
+  using SM = so3::MmaSmem<JW>;
+  if (analysis) {
+    const size_t smem = ((size_t)WPC * SM::DT_ROWS * SM::S + 2 * (size_t)WPC * 256) * sizeof(double);
+    auto k = so3::dwt_analysis_mma_kernel<JW, WPC>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl * split, batch);
+    cfg.blockDim = dim3(WPC * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SO3_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  } else {
+    const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
+    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<dim3(ncl * split, batch), WPC * 32, smem, st>>>(a, split);
+  }
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+template <int JW>
+int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+  const int warps = (n + JW - 1) / JW;
+  if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
+  if (warps >= 4 && warps % 4 == 0) return launch_dwt_mma_wpc<JW, 4>(analysis, a, warps / 4, ncl, batch, st);
+  if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2>(analysis, a, warps / 2, ncl, batch, st);
+  return launch_dwt_mma_wpc<JW, 1>(analysis, a, warps, ncl, batch, st);
 }
 
 template <bool ANALYSIS>
@@ -187,9 +237,19 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.spec_fstride = p->ngrid;
   a.coef_fstride = p->ncoef;
   a.cluster0 = (int)c0;
+  a.rc = p->d_rc;
+  a.rc_off = p->d_rc_off;
+  const unsigned ncl = (unsigned)(c1 - c0);
+  if (p->dwt_variant == SO3_DWT_MMA && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
+    switch (dwt_jw(p->n)) {
+      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
+    }
+  }
   const int jt = dwt_jt(p->n);
   const int threads = std::min(256, ((p->n + jt - 1) / jt + 31) / 32 * 32);
-  dim3 grid((unsigned)(c1 - c0), p->batch);
+  dim3 grid(ncl, p->batch);
   switch (jt) {
     case 1: if (ANALYSIS) so3::dwt_analysis_kernel<1><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<1><<<grid, threads, 0, st>>>(a); break;
     case 2: if (ANALYSIS) so3::dwt_analysis_kernel<2><<<grid, threads, 0, st>>>(a); else so3::dwt_synthesis_kernel<2><<<grid, threads, 0, st>>>(a); break;
@@ -303,6 +363,12 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   }
   const auto cl = host_clusters(b);
   p->nclusters = (int64_t)cl.size();
+  std::vector<long long> rc_off(cl.size());
+  long long rc_entries = 0;
+  for (size_t i = 0; i < cl.size(); ++i) {
+    rc_off[i] = rc_entries;
+    rc_entries += std::max(1, b - 1 - cl[i].m);
+  }
   std::vector<int2> bases(cl.size());
   std::vector<double2> lnorm(cl.size());
   for (size_t i = 0; i < cl.size(); ++i) {
@@ -331,6 +397,8 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   PLAN_ALLOC(p->d_w, n);
   PLAN_ALLOC(p->d_tw, n);
   PLAN_ALLOC(p->d_scratch, (size_t)p->ngrid * batch);
+  PLAN_ALLOC(p->d_rc, (size_t)3 * rc_entries);
+  PLAN_ALLOC(p->d_rc_off, cl.size());
 #undef PLAN_ALLOC
   cudaError_t e = cudaSuccess;
   e = e ? e : cudaMemcpy(p->d_bases, bases.data(), bases.size() * sizeof(int2), cudaMemcpyHostToDevice);
@@ -339,6 +407,12 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   e = e ? e : cudaMemcpy(p->d_logcs, logcs.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_rc_off, rc_off.data(), rc_off.size() * sizeof(long long), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    so3::rc_table_kernel<<<(unsigned)cl.size(), 128>>>(b, (int)cl.size(), p->d_bases, p->d_rc_off, p->d_rc);
+    e = cudaGetLastError();
+  }
+  e = e ? e : cudaDeviceSynchronize();
   if (e != cudaSuccess) { cleanup(); return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e)); }
   *out = p;
   return SO3_OK;
@@ -353,6 +427,8 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_w);
   cudaFree(p->d_tw);
   cudaFree(p->d_scratch);
+  cudaFree(p->d_rc);
+  cudaFree(p->d_rc_off);
   cudaFree(p->d_grid_stage);
   cudaFree(p->d_coef_stage);
   delete p;
@@ -363,6 +439,13 @@ int so3_plan_batch(so3_plan_t p) { return p ? p->batch : 0; }
 int so3_plan_device(so3_plan_t p) { return p ? p->device : -1; }
 int64_t so3_plan_device_bytes(so3_plan_t p) { return p ? p->bytes : 0; }
 void* so3_plan_scratch(so3_plan_t p) { return p ? p->d_scratch : nullptr; }
+
+int so3_plan_set_dwt_variant(so3_plan_t p, int variant) {
+  if (!p) return fail(SO3_ERR_INVALID, "null plan");
+  if (variant != SO3_DWT_MMA && variant != SO3_DWT_SIMT) return fail(SO3_ERR_INVALID, "unknown DWT variant");
+  p->dwt_variant = variant;
+  return SO3_OK;
+}
 
 #define CHECK_PLAN(p) \
   if (!(p)) return fail(SO3_ERR_INVALID, "null plan")

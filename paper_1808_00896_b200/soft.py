@@ -79,6 +79,29 @@ def cluster_for_base(m: int, mp: int) -> SymmetryCluster:
     return SymmetryCluster(kind, OrderPair(m, mp), tuple(members))
 
 
+def enumerate_clusters(bandwidth: int, partitioner: str = "kappa") -> list[SymmetryCluster]:
+    """All symmetry clusters below B in the reference's order (schedule.py:136-158).
+
+    "kappa": origin, axis, diagonal, then the kappa rectangle (integer divmod split,
+    schedule.py:59-90); "sigma": triangle order (schedule.py:40-52).  The GPU launch
+    order is cluster_schedule(); both cover the (2B-1)^2 order pairs exactly once.
+    """
+    b = validate_bandwidth(bandwidth)
+    if partitioner == "kappa":
+        bases = [(0, 0)] + [(m, 0) for m in range(1, b)] + [(m, m) for m in range(1, b)]
+        for kappa in range((b - 1) * (b - 2) // 2):
+            i, j = kappa // (b - 1) + 1, kappa % (b - 1) + 1
+            bases.append((b - i, b - j) if j > i else (i + 1, j))
+    elif partitioner == "sigma":
+        bases = []
+        for s in range(b * (b + 1) // 2):
+            m = int(math.floor(math.sqrt(2.0 * s + 0.25) - 0.5))
+            bases.append((m, s - m * (m + 1) // 2))
+    else:
+        raise ValueError(f"unknown partitioner {partitioner!r}")
+    return [cluster_for_base(m, mp) for m, mp in bases]
+
+
 @dataclass(frozen=True, eq=False)
 class SampleAngles:
     """Per-axis angles of the grid (reference quadrature.py:26-39)."""
@@ -169,18 +192,7 @@ class TransformPlan:
     @property
     def clusters(self) -> list[SymmetryCluster]:
         if self._clusters is None:
-            b = self.bandwidth
-            if self.partitioner == "kappa":       # schedule.py:146-153
-                bases = [(0, 0)] + [(m, 0) for m in range(1, b)] + [(m, m) for m in range(1, b)]
-                for kappa in range((b - 1) * (b - 2) // 2):
-                    i, j = kappa // (b - 1) + 1, kappa % (b - 1) + 1
-                    bases.append((b - i, b - j) if j > i else (i + 1, j))
-            else:                                  # schedule.py:154-157
-                bases = []
-                for s in range(b * (b + 1) // 2):
-                    m = int(math.floor(math.sqrt(2.0 * s + 0.25) - 0.5))
-                    bases.append((m, s - m * (m + 1) // 2))
-            self._clusters = [cluster_for_base(m, mp) for m, mp in bases]
+            self._clusters = enumerate_clusters(self.bandwidth, self.partitioner)
         return self._clusters
 
     @property
@@ -199,6 +211,13 @@ class TransformPlan:
         if self._handle is None:
             raise ValueError("plan has been released")
         return self._handle
+
+    def set_dwt_variant(self, variant: str) -> None:
+        """DWT kernel family: "mma" (default, FP64 DMMA) or "simt" (DFMA + warp butterfly)."""
+        code = {"mma": 0, "simt": 1}.get(variant)
+        if code is None:
+            raise ValueError(f"unknown DWT variant {variant!r}")
+        _native.check(_native.lib().so3_plan_set_dwt_variant(self.handle, code), "set_dwt_variant")
 
     @property
     def device_bytes(self) -> int:

@@ -1,0 +1,336 @@
+"""Parity of the CUDA path (through the C ABI) with the reference: golden vectors
+produced by the reference itself, the oracle on the same seeded inputs, and
+size-independent properties at BASELINE sizes.
+
+Tolerances (north_star: max relative coefficient error <= 1e-10, fp64):
+  * transforms vs reference/oracle: max |delta| / max |ref| <= 1e-12 (B <= 64),
+    and the per-slot form max |delta|/|ref| (reference bench.py:122-131) <= 1e-10;
+  * round trips: max abs error <= 1e-11 up to B=128 (reference test_soft.py:48-54
+    uses 1e-11 for B <= 16; acceptance criterion 3 uses abs < 1e-10, rel < 1e-6).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import so3_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+so3 = pytest.importorskip("paper_1808_00896_b200")
+
+SOFT_B = [1, 2, 3, 4, 5, 6, 8, 16]
+
+
+def rel_of_max(got, ref):
+    return float(np.abs(np.asarray(got) - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+def per_slot(got, ref):
+    return O.error_metrics(ref, np.asarray(got))[1]
+
+
+@pytest.fixture(scope="module", params=["mma", "simt"])
+def variant(request):
+    return request.param
+
+
+def plan_for(b, variant="mma", **kw):
+    p = so3.make_plan(b, **kw)
+    p.set_dwt_variant(variant)
+    return p
+
+
+# ---------------------------------------------------------------- golden vectors of the reference
+
+@pytest.mark.parametrize("b", SOFT_B)
+def test_inverse_matches_reference_golden(golden, b, variant):
+    g = golden(f"soft_b{b}.npz")
+    out = so3.ifsoft_sequential(so3.So3Coefficients(b, g["coeffs"]), plan_for(b, variant)).data
+    assert rel_of_max(out, g["inverse"]) < 1e-12
+    np.testing.assert_allclose(out, g["inverse"], rtol=0, atol=1e-12 * np.abs(g["inverse"]).max())
+
+
+@pytest.mark.parametrize("b", SOFT_B)
+def test_forward_matches_reference_golden(golden, b, variant):
+    g = golden(f"soft_b{b}.npz")
+    plan = plan_for(b, variant)
+    back = so3.fsoft_sequential(so3.So3SampleGrid(b, g["inverse"]), plan).data
+    assert rel_of_max(back, g["roundtrip"]) < 1e-12
+    assert per_slot(back, g["roundtrip"]) < 1e-10
+    raw = so3.fsoft_sequential(so3.So3SampleGrid(b, g["raw_grid"]), plan).data
+    assert rel_of_max(raw, g["forward_raw"]) < 1e-12
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_fast_matches_reference_direct_route(golden, b):
+    """Against the reference's O(B^6) closed-form route (soft.py:212-256; test_soft.py:30-45)."""
+    g = golden(f"soft_b{b}.npz")
+    plan = plan_for(b)
+    inv = so3.ifsoft_sequential(so3.So3Coefficients(b, g["coeffs"]), plan).data
+    np.testing.assert_allclose(inv, g["direct_inverse"], atol=1e-12)
+    fwd = so3.fsoft_sequential(so3.So3SampleGrid(b, g["raw_grid"]), plan).data
+    np.testing.assert_allclose(fwd, g["direct_forward"], atol=1e-12)
+
+
+# ---------------------------------------------------------------- oracle on seeded inputs
+
+@pytest.mark.parametrize("b", [7, 10, 12, 24, 32, 33, 64])
+def test_both_directions_match_oracle(b, variant):
+    rng = np.random.default_rng(b)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    plan = plan_for(b, variant)
+    g_ref = O.ifsoft(c, b)
+    g = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
+    assert rel_of_max(g, g_ref) < 1e-12
+    f_ref = O.fsoft(g_ref, b)
+    f = so3.fsoft_sequential(so3.So3SampleGrid(b, g_ref), plan).data
+    assert rel_of_max(f, f_ref) < 1e-12
+    assert per_slot(f, f_ref) < 1e-10
+
+
+def test_sampled_oracle_at_b256():
+    """B=256: FFT stage on sampled slices and DWT on sampled clusters vs the oracle, fed the
+    same inputs (SURVEY.md 8(c) sampled-oracle fallback for large B)."""
+    b, n = 256, 512
+    plan = plan_for(b)
+    rng = np.random.default_rng(256)
+    grid = rng.standard_normal(n ** 3) + 1j * rng.standard_normal(n ** 3)
+    gd = torch.from_numpy(grid).cuda()
+    spec = torch.empty_like(gd)
+    so3.fft_analysis(plan, gd, spec)
+    S = spec.cpu().numpy().reshape(n, n, n)        # [m][m'][j], weighted
+    w = O.beta_weights(b)
+    cube = grid.reshape(n, n, n)
+    for j in (0, 37, 255, 511):
+        ref = O.slice_dft(cube[:, j, :], +1) * w[j]
+        got = S[:, :, j].copy()
+        got[:, b] = ref[:, b]                      # column m' = B is never written (not needed)
+        assert rel_of_max(got, ref) < 1e-13
+    coeffs = torch.empty(O.n_coeffs(b), dtype=torch.complex128, device="cuda")
+    so3.dwt_analysis(plan, spec, coeffs)
+    got = coeffs.cpu().numpy()
+    betas = O.beta_nodes(b)
+    v = (2.0 * np.arange(b) + 1.0) / (8.0 * math.pi * b)
+    for (bm, bmp) in [(0, 0), (5, 0), (9, 9), (100, 37), (255, 254), (200, 3)]:
+        rows = O.recurrence_rows(bm, bmp, betas, b)
+        for (m, mp, tag) in O.cluster_members(bm, bmp):
+            col = O.analysis_column(O.member_matrix(rows, tag, bm, bmp, b), v[bm:], np.ones(n),
+                                    S[m % n, mp % n, :])
+            mine = got[O.pair_slots(m, mp, b)]
+            assert rel_of_max(mine, col) < 1e-12, (m, mp)
+
+
+# ---------------------------------------------------------------- stages and Wigner rows
+
+def test_wigner_rows_match_reference_golden(golden):
+    g = golden("wigner.npz")
+    for b in (16, 64):
+        plan = plan_for(b)
+        for (m, mp) in [(0, 0), (1, 0), (3, 3), (5, 2), (b - 1, 0), (b - 1, b - 2), (b // 2, b // 3)]:
+            rows = so3.wigner_rows(plan, m, mp).cpu().numpy()
+            np.testing.assert_allclose(rows, g[f"rows_b{b}_{m}_{mp}"], rtol=0, atol=1e-13)
+
+
+def test_wigner_rows_every_pair_against_closed_form():
+    b = 12
+    plan = plan_for(b)
+    betas = O.beta_nodes(b)
+    for m in range(-b + 1, b):
+        for mp in range(-b + 1, b):
+            rows = so3.wigner_rows(plan, m, mp).cpu().numpy()
+            lo = max(abs(m), abs(mp))
+            for i, l in enumerate(range(lo, b)):
+                np.testing.assert_allclose(rows[i], O.closed_form_d(l, m, mp, betas), atol=1e-12)
+
+
+def test_dwt_stage_matches_reference_columns(golden):
+    """Per-member dwt_apply / idwt_apply golden columns of the reference (dwt.py:109-125)."""
+    g = golden("wigner.npz")
+    for b in (16, 64):
+        n = 2 * b
+        plan = plan_for(b)
+        w = O.beta_weights(b)
+        for (bm, bmp) in [(0, 0), (1, 0), (3, 3), (5, 2), (b - 1, 0), (b - 1, b - 2), (b // 2, b // 3)]:
+            spec = np.zeros((n, n, n), dtype=np.complex128)
+            coef = np.zeros(O.n_coeffs(b), dtype=np.complex128)
+            for (m, mp, _) in O.cluster_members(bm, bmp):
+                spec[m % n, mp % n, :] = g[f"dwt_in_b{b}_{m}_{mp}"] * w     # K1 fuses w_j
+                coef[O.pair_slots(m, mp, b)] = g[f"idwt_in_b{b}_{m}_{mp}"]
+            sd = torch.from_numpy(spec.reshape(-1)).cuda()
+            cd = torch.empty(O.n_coeffs(b), dtype=torch.complex128, device="cuda")
+            so3.dwt_analysis(plan, sd, cd)
+            cd = cd.cpu().numpy()
+            sd2 = torch.zeros(n ** 3, dtype=torch.complex128, device="cuda")
+            so3.dwt_synthesis(plan, torch.from_numpy(coef).cuda(), sd2)
+            sd2 = sd2.cpu().numpy().reshape(n, n, n)
+            for (m, mp, _) in O.cluster_members(bm, bmp):
+                ref = g[f"dwt_out_b{b}_{m}_{mp}"]
+                assert rel_of_max(cd[O.pair_slots(m, mp, b)], ref) < 1e-12
+                ref2 = g[f"idwt_out_b{b}_{m}_{mp}"]
+                assert rel_of_max(sd2[m % n, mp % n, :], ref2) < 1e-12
+
+
+# ---------------------------------------------------------------- properties at BASELINE sizes
+
+@pytest.mark.parametrize("b,tol", [(128, 1e-11), (256, 1e-11)])
+def test_round_trip_large(b, tol, variant):
+    rng = np.random.default_rng(b)
+    c = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    plan = plan_for(b, variant)
+    back = so3.fsoft_sequential(so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan), plan).data
+    err = float((back - c).abs().max())
+    assert err < tol
+    rel = float(((back - c).abs() / c.abs()).max())
+    assert rel < 1e-8   # per-slot (min |c| ~ 1e-4 at these sizes); reference B=256: 8.3e-11
+
+
+@pytest.mark.slow
+def test_round_trip_b512():
+    b = 512
+    rng = np.random.default_rng(b)
+    c = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    plan = plan_for(b)
+    back = so3.fsoft_sequential(so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan), plan).data
+    assert float((back - c).abs().max()) < 1e-10
+    assert float((back - c).abs().max() / c.abs().max()) < 1e-12
+
+
+def test_linearity_b128():
+    b = 128
+    n3 = (2 * b) ** 3
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.standard_normal(n3) + 1j * rng.standard_normal(n3)).cuda()
+    y = torch.from_numpy(rng.standard_normal(n3) + 1j * rng.standard_normal(n3)).cuda()
+    a = 0.75 - 1.25j
+    plan = plan_for(b)
+    f = lambda z: so3.fsoft_sequential(so3.So3SampleGrid(b, z), plan).data
+    lhs = f(a * x + y)
+    rhs = a * f(x) + f(y)
+    assert float((lhs - rhs).abs().max() / rhs.abs().max()) < 1e-13
+
+
+def test_parseval_b64():
+    """(pi/B) sum w |f|^2 = sum |c|^2 8 pi^2/(2l+1) (reference test_soft.py:87-107)."""
+    b = 64
+    rng = np.random.default_rng(5)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    grid = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan_for(b)).data.reshape(2 * b, 2 * b, 2 * b)
+    w = O.beta_weights(b)
+    lhs = (math.pi / b) * np.sum(np.abs(grid) ** 2 * w[None, :, None])
+    ls = O.degree_of_slot(b)
+    rhs = np.sum(np.abs(c) ** 2 * 8 * math.pi ** 2 / (2 * ls + 1))
+    assert lhs == pytest.approx(rhs, rel=1e-12)
+
+
+def test_unit_coefficients_sample_wigner_D():
+    """Synthesis of a unit coefficient samples D^l_{mm'} (reference test_soft.py:61-70)."""
+    b = 4
+    plan = plan_for(b)
+    al, be = O.angle_nodes(b), O.beta_nodes(b)
+    for (l, m, mp) in [(0, 0, 0), (1, 1, -1), (2, -2, 1), (3, 3, 3), (3, -1, 2)]:
+        c = np.zeros(O.n_coeffs(b), dtype=np.complex128)
+        c[O.slot(l, m, mp)] = 1.0
+        grid = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data.reshape(2 * b, 2 * b, 2 * b)
+        for i in (0, 3):
+            for j in (0, 5):
+                for k in (1, 7):
+                    d = O.closed_form_d(l, m, mp, be[j])
+                    want = np.exp(-1j * m * al[i]) * d * np.exp(-1j * mp * al[k])
+                    assert abs(grid[i, j, k] - want) < 1e-12
+
+
+def test_constant_function_projects_to_lowest_harmonic():
+    b = 8
+    f = so3.fsoft_sequential(so3.So3SampleGrid(b, np.ones((2 * b) ** 3)), plan_for(b)).data
+    e = np.zeros_like(f)
+    e[0] = 1.0
+    np.testing.assert_allclose(f, e, atol=1e-12)
+
+
+# ---------------------------------------------------------------- API behaviour
+
+def test_numpy_and_torch_paths_identical_and_deterministic():
+    b = 32
+    rng = np.random.default_rng(1)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    plan = plan_for(b)
+    g1 = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
+    g2 = so3.ifsoft_parallel(so3.So3Coefficients(b, torch.from_numpy(c).cuda()), plan, 8).data.cpu().numpy()
+    np.testing.assert_array_equal(g1, g2)
+    f1 = so3.fsoft_sequential(so3.So3SampleGrid(b, g1), plan).data
+    f2 = so3.fsoft_parallel(so3.So3SampleGrid(b, g1), plan, 3).data
+    np.testing.assert_array_equal(f1, f2)
+
+
+def test_policies_and_partitioners_bit_identical():
+    b = 8
+    rng = np.random.default_rng(2)
+    grid = rng.standard_normal((2 * b) ** 3) + 1j * rng.standard_normal((2 * b) ** 3)
+    outs = [so3.fsoft_sequential(so3.So3SampleGrid(b, grid), so3.make_plan(b, pol, part)).data
+            for pol in ("streaming", "precomputed") for part in ("kappa", "sigma")]
+    for o in outs[1:]:
+        np.testing.assert_array_equal(o, outs[0])
+
+
+def test_plan_errors():
+    plan = plan_for(4)
+    with pytest.raises(ValueError):
+        so3.fsoft_sequential(so3.So3SampleGrid.zeros(5), plan)
+    with pytest.raises(ValueError):
+        so3.ifsoft_sequential(so3.So3Coefficients.zeros(5), plan)
+    with pytest.raises(ValueError):
+        so3.fsoft_parallel(so3.So3SampleGrid.zeros(4), plan, threads=0)
+    with pytest.raises(ValueError):
+        so3.dwt_analysis(plan, torch.zeros(512, dtype=torch.complex128, device="cuda"),
+                         torch.zeros(84, dtype=torch.complex128, device="cuda"), 0, 10 ** 6)
+    assert plan.bandwidth == 4 and len(plan.clusters) == 10
+    assert sum(len(c.members) for c in plan.clusters) == 7 ** 2
+
+
+def test_inputs_not_modified():
+    b = 8
+    rng = np.random.default_rng(3)
+    c = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    keep = c.clone()
+    plan = plan_for(b)
+    g = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
+    gk = g.clone()
+    so3.fsoft_sequential(so3.So3SampleGrid(b, g), plan)
+    assert torch.equal(c, keep) and torch.equal(g, gk)
+
+
+def test_batch_b32x64_matches_single_function_path():
+    """BASELINE configs[1]: B=32, 64 functions, N(0,1) scaled by 1/(1+l)."""
+    b, F = 32, 64
+    C = O.n_coeffs(b)
+    scale = 1.0 / (1.0 + O.degree_of_slot(b))
+    cs = []
+    for f in range(F):
+        rng = np.random.default_rng(32000 + f)
+        cs.append((rng.standard_normal(C) + 1j * rng.standard_normal(C)) * scale)
+    cs = np.stack(cs)
+    bplan = plan_for(b, batch=F)
+    grids = so3.ifsoft_batch(torch.from_numpy(cs).cuda(), bplan)
+    back = so3.fsoft_batch(grids, bplan).cpu().numpy()
+    assert np.abs(back - cs).max() < 1e-12
+    single = plan_for(b)
+    gn = grids.cpu().numpy()
+    for f in (0, 17, 63):
+        one = so3.ifsoft_sequential(so3.So3Coefficients(b, cs[f]), single).data
+        np.testing.assert_array_equal(one, gn[f])
+    for f in (0, 5):
+        assert rel_of_max(gn[f], O.ifsoft(cs[f], b)) < 1e-12
+
+
+def test_sofc_round_trip_through_transform(tmp_path):
+    b = 8
+    rng = np.random.default_rng(4)
+    c = so3.So3Coefficients(b, rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b)))
+    so3.write_coefficients(str(tmp_path / "c.sofc"), c)
+    plan = plan_for(b)
+    g = so3.ifsoft_sequential(so3.read_coefficients(str(tmp_path / "c.sofc")), plan)
+    so3.write_samples(str(tmp_path / "g.sofg"), g)
+    back = so3.fsoft_sequential(so3.read_samples(str(tmp_path / "g.sofg")), plan)
+    assert np.abs(back.data - c.data).max() < 1e-12
