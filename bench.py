@@ -372,7 +372,7 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(f"B{b}", {}).get(dom)
-    roof = {"kernel": f"{dom} (dwt_{'analysis' if dom == 'dwt_analysis' else 'synthesis'}_kernel)",
+    roof = {"kernel": f"{dom} (dwt_{'analysis' if dom == 'dwt_analysis' else 'synthesis'}_mma_kernel, DMMA)",
             "bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
             "peak_source": peaks["fp64_source"],
@@ -416,7 +416,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--bandwidth", "-B", type=int, default=DEFAULT_B)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--dwt-variant", choices=("mma", "simt"), default="mma")
+    ap.add_argument("--dwt-variant", choices=("mma", "mma2", "simt"), default="mma")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)

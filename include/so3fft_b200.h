@@ -106,12 +106,13 @@ int so3_ifsoft_host(so3_plan_t plan, const void* coeffs_host, void* samples_host
 
 /* Forward torus stage: for every beta slice the sign +1 2-D DFT
  * (fft.py:72-76 via soft.py:130-132) times the quadrature weight w_j, written
- * pair-major: spectrum_dev[f][m mod 2B][m' mod 2B][j] (column m' = B unwritten). */
+ * pair-major: spectrum_dev[f][m' mod 2B][m mod 2B][j] (rows m' = B unwritten).
+ * Uses the plan's pass-1 scratch; spectrum_dev must be a different buffer. */
 int so3_fft_analysis(so3_plan_t plan, const void* samples_dev, void* spectrum_dev, void* stream);
 
 /* Inverse torus stage: sign -1 2-D DFT per slice (soft.py:164-172) of
- * spectrum_dev[f][m][m'][j] (rows/columns at the Nyquist bin B read as zero).
- * spectrum_dev is used as scratch (overwritten). */
+ * spectrum_dev[f][m'][m][j] (entries at the Nyquist bin B read as zero).
+ * spectrum_dev is read only. */
 int so3_fft_synthesis(so3_plan_t plan, void* spectrum_dev, void* samples_dev, void* stream);
 
 /* Forward DWT (dwt.py:109-116 per member, soft.py:134-148) over clusters
@@ -121,17 +122,19 @@ int so3_dwt_analysis(so3_plan_t plan, const void* spectrum_dev, void* coeffs_dev
                      int64_t cluster_begin, int64_t cluster_end, void* stream);
 
 /* Inverse DWT (dwt.py:119-125 per member, soft.py:157-167) over clusters
- * [cluster_begin, cluster_end): writes spectrum_dev[f][m][m'][j] of their pairs. */
+ * [cluster_begin, cluster_end): writes spectrum_dev[f][m'][m][j] of their pairs. */
 int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_dev,
                       int64_t cluster_begin, int64_t cluster_end, void* stream);
 
-/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4 contraction) or
- * SO3_DWT_SIMT (DFMA + warp-butterfly reduction).  Same results to rounding. */
+/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4), SO3_DWT_MMA2 (DMMA,
+ * barrier-free ring reduction) or SO3_DWT_SIMT (DFMA + warp butterfly).  Same results
+ * to rounding. */
 #define SO3_DWT_MMA 0
 #define SO3_DWT_SIMT 1
+#define SO3_DWT_MMA2 2
 int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
 
-/* Scratch spectrum owned by the plan (device pointer, batch x (2B)^3 complex128). */
+/* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */
 void* so3_plan_scratch(so3_plan_t plan);
 
 /* Wigner rows d^l_{m,m'}(beta_j), l = max(|m|,|m'|)..B-1, j < 2B, for any pair

@@ -43,7 +43,7 @@ struct Member {
   int sl;        // sign exponent coefficient of l
   int par0;      // parity of sm*m + smp*m'
   int pm, pmp;   // member order pair
-  long long row; // (pm mod n) * n + (pmp mod n): row of the [m][m'][j] spectrum
+  long long row; // (pmp mod n) * n + (pm mod n): row of the [m'][m][j] spectrum
 };
 
 // Tags per cluster kind: origin {0}; axis {0,1,2,3}; diagonal {0,1,4,5}; full {0..7}.
@@ -63,7 +63,7 @@ __device__ __forceinline__ Member make_member(int m, int mp, int k, int n) {
   r.pm = R.tm_m * m + R.tm_mp * mp;
   r.pmp = R.tp_m * m + R.tp_mp * mp;
   const int bm = ((r.pm % n) + n) % n, bmp = ((r.pmp % n) + n) % n;
-  r.row = (long long)bm * n + bmp;
+  r.row = (long long)bmp * n + bm;
   return r;
 }
 

@@ -1,38 +1,44 @@
 // Torus DFT stage of FSOFT / iFSOFT (reference fft.py:35-76, soft.py:127-132, 164-172).
 //
-// The 2-D unnormalised DFT over (alpha, gamma) of every beta slice is done in
-// two passes over HBM, each a batch of 1-D FFTs of length N = 2B whose rows are
-// JB consecutive beta indices j:
+// The 2-D unnormalised DFT over (alpha, gamma) of every beta slice is done in two HBM
+// passes.  Every pass reads or writes FULL contiguous rows on one side and writes or reads
+// XB*16-byte chunks inside a single plane on the other side (a transposition that keeps
+// HBM locality; the strided-axis FFT that a plain 2-D FFT needs runs at < 50% of HBM):
 //
-//   ROW_FWD (K1a): grid[f][i][j][k]  --FFT_k(+1)-->  S[f][i][m'][j]     (transposing write)
-//   COL     (K1b): S[f][i][m'][j]    --FFT_i(+1)-->  S[f][m][m'][j] * w_j  (in place)
-//   COL     (K4a): S[f][m][m'][j]    --FFT_m(-1)-->  S[f][i][m'][j]        (in place)
-//   ROW_INV (K4b): S[f][i][m'][j]    --FFT_m'(-1)--> grid[f][i][j][k]   (transposing read)
+//   forward  K1a (RI): grid[i][j][k]  --FFT_k(+1)-->  T[j][m'][i]          rows (i,j) in
+//            K1b (RI): T[j][m'][i]    --FFT_i(+1)-->  X[m'][m][j] * w_j    rows (j,m') in
+//   inverse  K4a (CI): X[m'][m][j]    --FFT_m(-1)-->  T[j][m'][i]          rows (j,m') out
+//            K4b (CI): T[j][m'][i]    --FFT_m'(-1)--> grid[i][j][k]        rows (i,j) out
 //
-// so the DWT sees each order pair (m, m') as one contiguous vector over j.
-// Reads and writes are JB*16 bytes contiguous (or whole rows).  Each thread keeps
-// 16 points in registers and runs a radix-16 Stockham FFT whose stages exchange
-// through shared memory.  Twiddles come from a per-plan table tw[k] = exp(+2 pi i k / N).
-// Non power-of-two or tiny N use a direct O(N^2) DFT kernel (the reference also
-// falls back to a kernel-matrix product for those lengths, fft.py:51-54).
+// so the DWT sees each order pair as one contiguous vector over j (row m'*2B + m of X).
+// A CTA transforms XB rows; each thread keeps 16 points in registers and runs a radix-16
+// Stockham FFT whose stages exchange through padded shared memory.  Twiddles come from a
+// per-plan table tw[k] = exp(+2 pi i k / N).  Non power-of-two or tiny N use a direct
+// O(N^2) DFT (the reference also falls back to a kernel-matrix product, fft.py:51-54).
 #pragma once
 #include "common.cuh"
 
 namespace so3 {
 
-enum FftMode { ROW_FWD = 0, COL = 1, ROW_INV = 2 };
+enum FftMode { RI = 0, CI = 1 };   // rows in + chunks out / chunks in + rows out
 
+// A pass transforms rows indexed by (x, y, f): x in [0, X) grouped XB per CTA, y in [0, Y),
+// function f.  Element p of row (x, y) sits at  f*fs + y*sy + x*sx + p*sp  (in units of
+// complex128); the contiguous side has sp = 1 (rows) or sx = 1 (chunks over x).
 struct FftArgs {
-  int n;            // transform length N = 2B
-  int nyq;          // Nyquist bin B (treated as zero where the inverse reads it)
-  int J;            // beta slices held in this array (n on one GPU, the slab width when sharded)
-  int jbase;        // global index of local slice 0 (for the quadrature weights)
+  int n;                      // transform length N = 2B
+  int nyq;                    // Nyquist bin B
+  int X, Y;                   // row grid
+  int skip_y;                 // rows with y == skip_y are neither needed nor written (-1: none)
+  int zero_p;                 // input point index read as zero (-1: none), the Nyquist bin
+  int weight;                 // multiply outputs by w[jbase + x]
+  int jbase;
   const double2* src;
   double2* dst;
-  const double2* tw;     // N entries, exp(+2 pi i k / N)
-  const double* w;       // quadrature weights (forward COL only), global j
-  long long fstride_src; // per-function element strides (batch)
-  long long fstride_dst;
+  long long fs_in, sy_in, sx_in, sp_in;
+  long long fs_out, sy_out, sx_out, sp_out;
+  const double2* tw;          // N entries, exp(+2 pi i k / N)
+  const double* w;            // quadrature weights
 };
 
 // exp(SIGN * 2 pi i * Q / 16) * a, Q compile-time
@@ -107,6 +113,15 @@ __device__ __forceinline__ void dft_reg(double2 (&v)[R]) {
 // One radix-R Stockham stage with span NS (product of the radices before it).
 // Thread t owns butterflies b = t + q*N/16 (q < 16/R); butterfly b reads points
 // b + r*N/R (register slot q + r*16/R) and writes b/NS*NS*R + b%NS + r*NS.
+// Shared-memory row layout of the exchange: one pad slot per 16 points plus 8/JB (min 1) per
+// row keeps every stage's 16-byte stores and loads free of bank conflicts for the thread
+// mapping tid = jl + JB*t (checked by simulation for all N, JB used here).
+__device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
+template <int N, int JB>
+struct RowLayout {
+  static constexpr int SIZE = N + N / 16 + (JB >= 8 ? 1 : 8 / JB);
+};
+
 template <int N, int R, int NS, int SIGN, bool LAST>
 __device__ __forceinline__ void stockham_stage(double2 (&v)[16], int t, const double2* __restrict__ tw,
                                                double2* __restrict__ row) {
@@ -133,7 +148,7 @@ __device__ __forceinline__ void stockham_stage(double2 (&v)[16], int t, const do
     } else {
       const int base = (b / NS) * NS * R + (b & (NS - 1));
 #pragma unroll
-      for (int r = 0; r < R; ++r) row[base + r * NS] = u[r];
+      for (int r = 0; r < R; ++r) row[pidx(base + r * NS)] = u[r];
     }
   }
 }
@@ -158,7 +173,7 @@ __device__ __forceinline__ void fft_rows(double2 (&v)[16], int t, const double2*
     stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = row[t + e * (N / 16)];
+    for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
     __syncthreads();
     if constexpr (RX::N16 == 1) {
       stockham_stage<N, RX::REM, 16, SIGN, true>(v, t, tw, row);
@@ -168,106 +183,88 @@ __device__ __forceinline__ void fft_rows(double2 (&v)[16], int t, const double2*
       stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = row[t + e * (N / 16)];
+      for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
       __syncthreads();
       stockham_stage<N, RX::REM, 256, SIGN, true>(v, t, tw, row);
     } else {  // N16 == 3 (N = 4096)
       stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = row[t + e * (N / 16)];
+      for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
       __syncthreads();
       stockham_stage<N, 16, 256, SIGN, true>(v, t, tw, row);
     }
   }
 }
 
-// Element (row jl, point p) addresses of the three modes.  blockIdx: x = j block, y = i / m' / m row, z = function.
-template <int MODE>
-__device__ __forceinline__ long long src_index(const FftArgs& a, int y, int jj, int p) {
-  const long long n = a.n;
-  if constexpr (MODE == ROW_FWD) return ((long long)y * a.J + jj) * n + p;          // grid[i][j][k=p]
-  else if constexpr (MODE == COL) return ((long long)p * n + y) * a.J + jj;          // S[i=p][m'][j]
-  else return ((long long)y * n + p) * a.J + jj;                                      // S[i][m'=p][j]
-}
-template <int MODE>
-__device__ __forceinline__ long long dst_index(const FftArgs& a, int y, int jj, int p) {
-  const long long n = a.n;
-  if constexpr (MODE == ROW_FWD) return ((long long)y * n + p) * a.J + jj;           // S[i][m'=p][j]
-  else if constexpr (MODE == COL) return ((long long)p * n + y) * a.J + jj;          // S[m=p][m'][j]
-  else return ((long long)y * a.J + jj) * n + p;                                      // grid[i][j][k=p]
-}
-
-// Stockham path: N in {16..4096} power of two, JB rows per CTA, JB*N/16 threads.
-template <int N, int JB, int SIGN, int MODE>
-__global__ void __launch_bounds__(JB * N / 16) fft_pass_kernel(FftArgs a) {
+// Stockham path: N in {16..2048} power of two, XB rows per CTA, XB*N/16 threads (tid = xl + XB*t).
+template <int N, int XB, int SIGN, int MINB = (XB * N / 16 <= 256 ? 2 : 1)>
+__global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) {
   extern __shared__ double2 smem[];
   constexpr int TPR = N / 16;  // threads per row
   const int tid = threadIdx.x;
-  const int jl = tid % JB, t = tid / JB;
+  const int xl = tid % XB, t = tid / XB;
   const int y = blockIdx.y;
-  const int jj = blockIdx.x * JB + jl;
-  const bool jvalid = jj < a.J;
-  const double2* src = a.src + (long long)blockIdx.z * a.fstride_src;
-  double2* dst = a.dst + (long long)blockIdx.z * a.fstride_dst;
-  double2* row = smem + jl * (N + 1);
-  // inverse column pass: the m' = B column is never read downstream (ROW_INV zeroes it)
-  if constexpr (MODE == COL && SIGN < 0) { if (y == a.nyq) return; }
-  if constexpr (MODE == COL && SIGN > 0) { if (y == a.nyq) return; }   // forward: DWT never reads m' = B
+  const int x = blockIdx.x * XB + xl;
+  if (y == a.skip_y) return;   // uniform per CTA
+  const bool xvalid = x < a.X;
+  const long long f = blockIdx.z;
+  const double2* src = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)x * a.sx_in;
+  double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)x * a.sx_out;
+  double2* row = smem + xl * RowLayout<N, XB>::SIZE;
 
   double2 v[16];
 #pragma unroll
   for (int e = 0; e < 16; ++e) {
     const int p = t + e * TPR;
-    double2 z = make_double2(0.0, 0.0);
-    bool zero = !jvalid;
-    if constexpr (SIGN < 0) zero = zero || (p == a.nyq);   // Nyquist bins of the spectrum are zero (soft.py:164)
-    if (!zero) z = src[src_index<MODE>(a, y, jj, p)];
-    v[e] = z;
+    const bool zero = !xvalid || p == a.zero_p;
+    v[e] = zero ? make_double2(0.0, 0.0) : src[(long long)p * a.sp_in];
   }
   fft_rows<N, SIGN>(v, t, a.tw, row);
-  double wj = 1.0;
-  if constexpr (MODE == COL && SIGN > 0) { if (jvalid) wj = __ldg(&a.w[a.jbase + jj]); }
-  if (jvalid) {
+  double wx = 1.0;
+  if (a.weight && xvalid) wx = __ldg(&a.w[a.jbase + x]);
+  if (xvalid) {
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const int p = t + e * TPR;
       double2 z = v[e];
-      if constexpr (MODE == COL && SIGN > 0) { z.x *= wj; z.y *= wj; }
-      dst[dst_index<MODE>(a, y, jj, p)] = z;
+      z.x *= wx;
+      z.y *= wx;
+      dst[(long long)p * a.sp_out] = z;
     }
   }
 }
 
-// Direct DFT for non power-of-two or N < 16.  A CTA owns (row y, JC consecutive j) and
-// stages those JC length-N rows in shared memory before writing, so COL stays in place.
-template <int SIGN, int MODE>
-__global__ void __launch_bounds__(256) dft_direct_kernel(FftArgs a, int JC) {
+// Direct DFT for non power-of-two or N < 16: a CTA stages XC rows in shared memory and
+// computes every output point of them (O(N^2) per row).
+template <int SIGN>
+__global__ void __launch_bounds__(256) dft_direct_kernel(FftArgs a, int XC) {
   extern __shared__ double2 col[];
   const int y = blockIdx.y;
+  if (y == a.skip_y) return;
   const int n = a.n;
-  const int j0 = blockIdx.x * JC;
-  const int jc = min(JC, a.J - j0);
-  const double2* src = a.src + (long long)blockIdx.z * a.fstride_src;
-  double2* dst = a.dst + (long long)blockIdx.z * a.fstride_dst;
-  if constexpr (MODE == COL) { if (y == a.nyq) return; }
-  for (int idx = threadIdx.x; idx < jc * n; idx += blockDim.x) {
-    const int jl = idx % jc, p = idx / jc;
+  const int x0 = blockIdx.x * XC;
+  const int xc = min(XC, a.X - x0);
+  const long long f = blockIdx.z;
+  const double2* src = a.src + f * a.fs_in + (long long)y * a.sy_in;
+  double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out;
+  for (int idx = threadIdx.x; idx < xc * n; idx += blockDim.x) {
+    const int xl = idx % xc, p = idx / xc;
     double2 z = make_double2(0.0, 0.0);
-    if (!(SIGN < 0 && p == a.nyq)) z = src[src_index<MODE>(a, y, j0 + jl, p)];
-    col[p * JC + jl] = z;
+    if (p != a.zero_p) z = src[(long long)(x0 + xl) * a.sx_in + (long long)p * a.sp_in];
+    col[p * XC + xl] = z;
   }
   __syncthreads();
-  for (int idx = threadIdx.x; idx < jc * n; idx += blockDim.x) {
-    const int jl = idx % jc, q = idx / jc;
+  for (int idx = threadIdx.x; idx < xc * n; idx += blockDim.x) {
+    const int xl = idx % xc, q = idx / xc;
     double2 acc = make_double2(0.0, 0.0);
     for (int p = 0; p < n; ++p) {
       double2 w = __ldg(&a.tw[(int)(((long long)p * q) % n)]);
       if (SIGN < 0) w.y = -w.y;
-      acc = cadd(acc, cmul(col[p * JC + jl], w));
+      acc = cadd(acc, cmul(col[p * XC + xl], w));
     }
-    if constexpr (MODE == COL && SIGN > 0) { const double wj = a.w[a.jbase + j0 + jl]; acc.x *= wj; acc.y *= wj; }
-    dst[dst_index<MODE>(a, y, j0 + jl, q)] = acc;
+    if (a.weight) { const double wx = a.w[a.jbase + x0 + xl]; acc.x *= wx; acc.y *= wx; }
+    dst[(long long)(x0 + xl) * a.sx_out + (long long)q * a.sp_out] = acc;
   }
 }
 

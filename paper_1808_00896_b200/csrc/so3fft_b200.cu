@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +20,7 @@
 #include "common.cuh"
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
+#include "dwt_mma2.cuh"
 #include "fft.cuh"
 
 namespace {
@@ -92,7 +94,8 @@ struct so3_plan_s {
   double4* d_logcs = nullptr;
   double* d_w = nullptr;
   double2* d_tw = nullptr;
-  double2* d_scratch = nullptr;
+  double2* d_scratch = nullptr;      // T: pass-1 output / pass-2 input
+  double2* d_spec = nullptr;         // X: pair-major spectrum [m'][m][j]
   double* d_rc = nullptr;            // recurrence coefficient table
   long long* d_rc_off = nullptr;
   // staging for the host-buffer entry points
@@ -100,69 +103,102 @@ struct so3_plan_s {
   double2* d_coef_stage = nullptr;
   int64_t bytes = 0;
   int dwt_variant = SO3_DWT_MMA;
+  int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
+  int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
 };
 
 // ------------------------------------------------------------------ launches
 
 namespace {
 
-template <int N, int JB>
-int launch_fft_pow2(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
-  const int threads = JB * N / 16;
-  const size_t smem = (size_t)JB * (N + 1) * sizeof(double2);
-  dim3 grid((a.J + JB - 1) / JB, a.n, batch);
-  void (*k)(so3::FftArgs) = nullptr;
-  if (mode == so3::ROW_FWD) k = so3::fft_pass_kernel<N, JB, +1, so3::ROW_FWD>;
-  else if (mode == so3::ROW_INV) k = so3::fft_pass_kernel<N, JB, -1, so3::ROW_INV>;
-  else if (sign > 0) k = so3::fft_pass_kernel<N, JB, +1, so3::COL>;
-  else k = so3::fft_pass_kernel<N, JB, -1, so3::COL>;
+template <int N, int XB>
+int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
+  const int threads = XB * N / 16;
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
+  dim3 grid((a.X + XB - 1) / XB, a.Y, batch);
+  void (*k)(so3::FftArgs) = sign > 0 ? so3::fft_pass_kernel<N, XB, +1> : so3::fft_pass_kernel<N, XB, -1>;
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, threads, smem, st>>>(a);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
 
-int launch_fft_direct(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
-  const int JC = std::max(1, std::min(a.J, 2048 / a.n));
-  const size_t smem = (size_t)JC * a.n * sizeof(double2);
-  dim3 grid((a.J + JC - 1) / JC, a.n, batch);
-  void (*k)(so3::FftArgs, int) = nullptr;
-  if (mode == so3::ROW_FWD) k = so3::dft_direct_kernel<+1, so3::ROW_FWD>;
-  else if (mode == so3::ROW_INV) k = so3::dft_direct_kernel<-1, so3::ROW_INV>;
-  else if (sign > 0) k = so3::dft_direct_kernel<+1, so3::COL>;
-  else k = so3::dft_direct_kernel<-1, so3::COL>;
+int launch_fft_direct(const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
+  const int XC = std::max(1, std::min(a.X, 2048 / a.n));
+  const size_t smem = (size_t)XC * a.n * sizeof(double2);
+  dim3 grid((a.X + XC - 1) / XC, a.Y, batch);
+  void (*k)(so3::FftArgs, int) = sign > 0 ? so3::dft_direct_kernel<+1> : so3::dft_direct_kernel<-1>;
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<grid, 256, smem, st>>>(a, JC);
+  k<<<grid, 256, smem, st>>>(a, XC);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
 
-int launch_fft(const so3::FftArgs& a, int mode, int sign, int batch, cudaStream_t st) {
-  switch (a.n) {
-    case 16: return launch_fft_pow2<16, 16>(a, mode, sign, batch, st);
-    case 32: return launch_fft_pow2<32, 32>(a, mode, sign, batch, st);
-    case 64: return launch_fft_pow2<64, 32>(a, mode, sign, batch, st);
-    case 128: return launch_fft_pow2<128, 32>(a, mode, sign, batch, st);
-    case 256: return launch_fft_pow2<256, 16>(a, mode, sign, batch, st);
-    case 512: return launch_fft_pow2<512, 8>(a, mode, sign, batch, st);
-    case 1024: return launch_fft_pow2<1024, 4>(a, mode, sign, batch, st);
-    case 2048: return launch_fft_pow2<2048, 2>(a, mode, sign, batch, st);
-    default: return launch_fft_direct(a, mode, sign, batch, st);
+// XB (rows per CTA) = the chunk width on the transposed side (XB * 16 bytes).
+template <int N>
+int launch_fft_xb(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int xb) {
+  switch (xb) {
+    case 2: return launch_fft_pow2<N, 2>(a, sign, batch, st);
+    case 4: return launch_fft_pow2<N, 4>(a, sign, batch, st);
+    case 8: return launch_fft_pow2<N, 8>(a, sign, batch, st);
+    default: return launch_fft_pow2<N, 16>(a, sign, batch, st);
   }
 }
 
-so3::FftArgs fft_args(const so3_plan_s* p, const void* src, void* dst) {
+int launch_fft(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int xb_override = 0) {
+  switch (a.n) {
+    case 16: return launch_fft_pow2<16, 16>(a, sign, batch, st);
+    case 32: return launch_fft_pow2<32, 32>(a, sign, batch, st);
+    case 64: return launch_fft_pow2<64, 32>(a, sign, batch, st);
+    case 128: return launch_fft_pow2<128, 32>(a, sign, batch, st);
+    case 256: return launch_fft_xb<256>(a, sign, batch, st, xb_override ? xb_override : 4);
+    case 512: return launch_fft_xb<512>(a, sign, batch, st, xb_override ? xb_override : 4);
+    case 1024: return launch_fft_xb<1024>(a, sign, batch, st, xb_override ? xb_override : 4);
+    case 2048: return launch_fft_pow2<2048, 2>(a, sign, batch, st);
+    default: return launch_fft_direct(a, sign, batch, st);
+  }
+}
+
+// The four passes (see fft.cuh).  n = 2B; all strides in complex128 units.
+so3::FftArgs fft_pass_args(const so3_plan_s* p, int pass, const void* src, void* dst) {
+  const long long n = p->n, n2 = n * n;
   so3::FftArgs a;
   a.n = p->n;
   a.nyq = p->B;
-  a.J = p->n;
+  a.X = p->n;
+  a.Y = p->n;
+  a.skip_y = -1;
+  a.zero_p = -1;
+  a.weight = 0;
   a.jbase = 0;
   a.src = static_cast<const double2*>(src);
   a.dst = static_cast<double2*>(dst);
+  a.fs_in = a.fs_out = p->ngrid;
   a.tw = p->d_tw;
   a.w = p->d_w;
-  a.fstride_src = p->ngrid;
-  a.fstride_dst = p->ngrid;
+  switch (pass) {
+    case 0:   // K1a: grid[i][j][k] (x=i, y=j, p=k) -> T[j][m'][i]
+      a.sx_in = n2; a.sy_in = n; a.sp_in = 1;
+      a.sx_out = 1; a.sy_out = n2; a.sp_out = n;
+      break;
+    case 1:   // K1b: T[j][m'][i] (x=j, y=m', p=i) -> X[m'][m][j] * w_j
+      a.sx_in = n2; a.sy_in = n; a.sp_in = 1;
+      a.sx_out = 1; a.sy_out = n2; a.sp_out = n;
+      a.skip_y = p->B;   // the DWT never reads m' = B
+      a.weight = 1;
+      break;
+    case 2:   // K4a: X[m'][m][j] (x=j, y=m', p=m) -> T[j][m'][i]
+      a.sx_in = 1; a.sy_in = n2; a.sp_in = n;
+      a.sx_out = n2; a.sy_out = n; a.sp_out = 1;
+      a.zero_p = p->B;   // row m = B of the spectrum is zero (soft.py:164)
+      a.skip_y = p->B;   // column m' = B is zero: K4b reads it as zero instead
+      break;
+    default:  // K4b: T[j][m'][i] (x=i, y=j, p=m') -> grid[i][j][k]
+      a.sx_in = 1; a.sy_in = n2; a.sp_in = n;
+      a.sx_out = n2; a.sy_out = n; a.sp_out = 1;
+      a.zero_p = p->B;
+      break;
+  }
   return a;
 }
 
@@ -202,7 +238,7 @@ int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned
     SO3_CUDA(cudaLaunchKernelEx(&cfg, k, a));
   } else {
     const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
-    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC>;
+    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2)>;
     SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<dim3(ncl * split, batch), WPC * 32, smem, st>>>(a, split);
   }
@@ -213,10 +249,31 @@ int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned
 template <int JW>
 int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
   const int warps = (n + JW - 1) / JW;
-  if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
+  if (warps > (analysis ? 8 : 16)) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
   if (warps >= 4 && warps % 4 == 0) return launch_dwt_mma_wpc<JW, 4>(analysis, a, warps / 4, ncl, batch, st);
   if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2>(analysis, a, warps / 2, ncl, batch, st);
   return launch_dwt_mma_wpc<JW, 1>(analysis, a, warps, ncl, batch, st);
+}
+
+template <int JW>
+int launch_dwt_mma2(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+  using K = so3::Mma2<JW>;
+  const int warps = (n + JW - 1) / JW;
+  if (analysis) {
+    if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA2 analysis kernel");
+    const size_t smem = ((size_t)warps * K::ana_dt_doubles + (size_t)K::R * warps * 128) * sizeof(double);
+    auto k = so3::dwt_analysis_mma2_kernel<JW>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<dim3(ncl, batch), warps * 32, smem, st>>>(a);
+  } else {
+    const int split = (warps + 3) / 4;
+    const size_t smem = 4 * K::syn_warp_doubles * sizeof(double);
+    auto k = so3::dwt_synthesis_mma2_kernel<JW>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<dim3(ncl * split, batch), 128, smem, st>>>(a, split);
+  }
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
 }
 
 template <bool ANALYSIS>
@@ -240,7 +297,20 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.rc = p->d_rc;
   a.rc_off = p->d_rc_off;
   const unsigned ncl = (unsigned)(c1 - c0);
-  if (p->dwt_variant == SO3_DWT_MMA && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
+  if (p->dwt_variant == SO3_DWT_MMA2 && p->n <= 1024) {
+    const int jw = ANALYSIS ? (p->n >= 1024 ? 128 : p->n >= 512 ? 64 : 32)
+                            : (p->n >= 512 ? 128 : p->n >= 256 ? 64 : 32);
+    switch (jw) {
+      case 128: return launch_dwt_mma2<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      case 64: return launch_dwt_mma2<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      default: return launch_dwt_mma2<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
+    }
+  }
+  if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && p->syn_jw && (p->n + p->syn_jw - 1) / p->syn_jw <= 16) {
+    if (p->syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
+    if (p->syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
+  }
+  if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
       case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
       case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
@@ -343,6 +413,9 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   p->ncoef = so3_coeff_count(b);
   p->ngrid = so3_grid_count(b);
   cudaGetDevice(&p->device);
+  if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
+  if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
+  if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
   const int n = p->n;
 
   std::vector<double> w(n), cosb(n);
@@ -397,6 +470,7 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   PLAN_ALLOC(p->d_w, n);
   PLAN_ALLOC(p->d_tw, n);
   PLAN_ALLOC(p->d_scratch, (size_t)p->ngrid * batch);
+  PLAN_ALLOC(p->d_spec, (size_t)p->ngrid * batch);
   PLAN_ALLOC(p->d_rc, (size_t)3 * rc_entries);
   PLAN_ALLOC(p->d_rc_off, cl.size());
 #undef PLAN_ALLOC
@@ -427,6 +501,7 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_w);
   cudaFree(p->d_tw);
   cudaFree(p->d_scratch);
+  cudaFree(p->d_spec);
   cudaFree(p->d_rc);
   cudaFree(p->d_rc_off);
   cudaFree(p->d_grid_stage);
@@ -438,11 +513,12 @@ int so3_plan_bandwidth(so3_plan_t p) { return p ? p->B : 0; }
 int so3_plan_batch(so3_plan_t p) { return p ? p->batch : 0; }
 int so3_plan_device(so3_plan_t p) { return p ? p->device : -1; }
 int64_t so3_plan_device_bytes(so3_plan_t p) { return p ? p->bytes : 0; }
-void* so3_plan_scratch(so3_plan_t p) { return p ? p->d_scratch : nullptr; }
+void* so3_plan_scratch(so3_plan_t p) { return p ? p->d_spec : nullptr; }
 
 int so3_plan_set_dwt_variant(so3_plan_t p, int variant) {
   if (!p) return fail(SO3_ERR_INVALID, "null plan");
-  if (variant != SO3_DWT_MMA && variant != SO3_DWT_SIMT) return fail(SO3_ERR_INVALID, "unknown DWT variant");
+  if (variant != SO3_DWT_MMA && variant != SO3_DWT_SIMT && variant != SO3_DWT_MMA2)
+    return fail(SO3_ERR_INVALID, "unknown DWT variant");
   p->dwt_variant = variant;
   return SO3_OK;
 }
@@ -454,24 +530,22 @@ int so3_plan_set_dwt_variant(so3_plan_t p, int variant) {
 
 int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
-  if (samples == spectrum) return fail(SO3_ERR_INVALID, "fft_analysis cannot run in place");
+  if (samples == spectrum || spectrum == p->d_scratch)
+    return fail(SO3_ERR_INVALID, "fft_analysis: spectrum must not alias the samples or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  so3::FftArgs a = fft_args(p, samples, spectrum);
-  int rc = launch_fft(a, so3::ROW_FWD, +1, p->batch, st);      // K1a: gamma axis, transposing write
+  int rc = launch_fft(fft_pass_args(p, 0, samples, p->d_scratch), +1, p->batch, st, p->fft_wide);
   if (rc) return rc;
-  a = fft_args(p, spectrum, spectrum);
-  return launch_fft(a, so3::COL, +1, p->batch, st);            // K1b: alpha axis * w_j, in place
+  return launch_fft(fft_pass_args(p, 1, p->d_scratch, spectrum), +1, p->batch, st, p->fft_wide);
 }
 
 int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
-  if (samples == spectrum) return fail(SO3_ERR_INVALID, "fft_synthesis cannot run in place");
+  if (samples == spectrum || spectrum == p->d_scratch || samples == p->d_scratch)
+    return fail(SO3_ERR_INVALID, "fft_synthesis: buffers must not alias each other or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  so3::FftArgs a = fft_args(p, spectrum, spectrum);
-  int rc = launch_fft(a, so3::COL, -1, p->batch, st);          // K4a: m -> alpha, in place
+  int rc = launch_fft(fft_pass_args(p, 2, spectrum, p->d_scratch), -1, p->batch, st, p->fft_wide);
   if (rc) return rc;
-  a = fft_args(p, spectrum, samples);
-  return launch_fft(a, so3::ROW_INV, -1, p->batch, st);        // K4b: m' -> gamma, transposing read
+  return launch_fft(fft_pass_args(p, 3, p->d_scratch, samples), -1, p->batch, st, p->fft_wide);
 }
 
 int so3_dwt_analysis(so3_plan_t p, const void* spectrum, void* coeffs, int64_t c0, int64_t c1, void* stream) {
@@ -487,16 +561,16 @@ int so3_dwt_synthesis(so3_plan_t p, const void* coeffs, void* spectrum, int64_t 
 
 int so3_fsoft(so3_plan_t p, const void* samples, void* coeffs, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(coeffs);
-  int rc = so3_fft_analysis(p, samples, p->d_scratch, stream);
+  int rc = so3_fft_analysis(p, samples, p->d_spec, stream);
   if (rc) return rc;
-  return so3_dwt_analysis(p, p->d_scratch, coeffs, 0, p->nclusters, stream);
+  return so3_dwt_analysis(p, p->d_spec, coeffs, 0, p->nclusters, stream);
 }
 
 int so3_ifsoft(so3_plan_t p, const void* coeffs, void* samples, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(coeffs);
-  int rc = so3_dwt_synthesis(p, coeffs, p->d_scratch, 0, p->nclusters, stream);
+  int rc = so3_dwt_synthesis(p, coeffs, p->d_spec, 0, p->nclusters, stream);
   if (rc) return rc;
-  return so3_fft_synthesis(p, p->d_scratch, samples, stream);
+  return so3_fft_synthesis(p, p->d_spec, samples, stream);
 }
 
 static int ensure_stage(so3_plan_t p) {

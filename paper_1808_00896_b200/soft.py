@@ -213,8 +213,8 @@ class TransformPlan:
         return self._handle
 
     def set_dwt_variant(self, variant: str) -> None:
-        """DWT kernel family: "mma" (default, FP64 DMMA) or "simt" (DFMA + warp butterfly)."""
-        code = {"mma": 0, "simt": 1}.get(variant)
+        """DWT kernel family: "mma" (default: FP64 DMMA), "mma2" (DMMA, pipelined) or "simt" (DFMA)."""
+        code = {"mma": 0, "simt": 1, "mma2": 2}.get(variant)
         if code is None:
             raise ValueError(f"unknown DWT variant {variant!r}")
         _native.check(_native.lib().so3_plan_set_dwt_variant(self.handle, code), "set_dwt_variant")
@@ -374,13 +374,13 @@ def _ptr(t) -> ctypes.c_void_p:
 
 
 def fft_analysis(plan: TransformPlan, samples, spectrum) -> None:
-    """K1: weighted torus spectrum spectrum[f][m][m'][j] of device samples (fft.py:72-76, soft.py:130-132)."""
+    """K1: weighted torus spectrum spectrum[f][m'][m][j] of device samples (fft.py:72-76, soft.py:130-132)."""
     _native.check(_native.lib().so3_fft_analysis(plan.handle, _ptr(samples), _ptr(spectrum), _stream(plan)),
                   "fft_analysis")
 
 
 def fft_synthesis(plan: TransformPlan, spectrum, samples) -> None:
-    """K4: samples from spectrum[f][m][m'][j] (soft.py:164-172); spectrum is overwritten."""
+    """K4: samples from spectrum[f][m'][m][j] (soft.py:164-172); spectrum is read only."""
     _native.check(_native.lib().so3_fft_synthesis(plan.handle, _ptr(spectrum), _ptr(samples), _stream(plan)),
                   "fft_synthesis")
 

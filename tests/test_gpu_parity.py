@@ -31,7 +31,7 @@ def per_slot(got, ref):
     return O.error_metrics(ref, np.asarray(got))[1]
 
 
-@pytest.fixture(scope="module", params=["mma", "simt"])
+@pytest.fixture(scope="module", params=["mma2", "mma", "simt"])
 def variant(request):
     return request.param
 
@@ -100,7 +100,7 @@ def test_sampled_oracle_at_b256():
     gd = torch.from_numpy(grid).cuda()
     spec = torch.empty_like(gd)
     so3.fft_analysis(plan, gd, spec)
-    S = spec.cpu().numpy().reshape(n, n, n)        # [m][m'][j], weighted
+    S = spec.cpu().numpy().reshape(n, n, n).transpose(1, 0, 2)   # stored [m'][m][j] -> [m][m'][j]
     w = O.beta_weights(b)
     cube = grid.reshape(n, n, n)
     for j in (0, 37, 255, 511):
@@ -156,7 +156,7 @@ def test_dwt_stage_matches_reference_columns(golden):
             spec = np.zeros((n, n, n), dtype=np.complex128)
             coef = np.zeros(O.n_coeffs(b), dtype=np.complex128)
             for (m, mp, _) in O.cluster_members(bm, bmp):
-                spec[m % n, mp % n, :] = g[f"dwt_in_b{b}_{m}_{mp}"] * w     # K1 fuses w_j
+                spec[mp % n, m % n, :] = g[f"dwt_in_b{b}_{m}_{mp}"] * w     # [m'][m][j]; K1 fuses w_j
                 coef[O.pair_slots(m, mp, b)] = g[f"idwt_in_b{b}_{m}_{mp}"]
             sd = torch.from_numpy(spec.reshape(-1)).cuda()
             cd = torch.empty(O.n_coeffs(b), dtype=torch.complex128, device="cuda")
@@ -164,7 +164,7 @@ def test_dwt_stage_matches_reference_columns(golden):
             cd = cd.cpu().numpy()
             sd2 = torch.zeros(n ** 3, dtype=torch.complex128, device="cuda")
             so3.dwt_synthesis(plan, torch.from_numpy(coef).cuda(), sd2)
-            sd2 = sd2.cpu().numpy().reshape(n, n, n)
+            sd2 = sd2.cpu().numpy().reshape(n, n, n).transpose(1, 0, 2)
             for (m, mp, _) in O.cluster_members(bm, bmp):
                 ref = g[f"dwt_out_b{b}_{m}_{mp}"]
                 assert rel_of_max(cd[O.pair_slots(m, mp, b)], ref) < 1e-12
