@@ -9,10 +9,13 @@ transforms; ``value`` = transforms/s of the whole job.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--bandwidth B]
   python bench.py --impl reference ...     # CPU reference arm (oracle port, all host cores)
 
-Rank 0 prints ONE JSON line.  Under torchrun (N > 1) each rank runs an
-independent replica of the single-GPU step (see DESIGN.md, "Multi-GPU");
-the timed region is bracketed by a barrier + synchronize and the max over
-ranks is reported.
+Rank 0 prints ONE JSON line.  Under torchrun (N > 1) the default is the
+sharded pipeline: ONE transform split over the N GPUs (beta slabs for the
+torus FFT, cost-balanced cluster groups for the DWT, one NCCL all-to-all per
+direction; paper_1808_00896_b200/distributed.py), i.e. strong scaling;
+``--mode replicas`` runs N independent single-GPU replicas instead.  The timed
+region is bracketed by a barrier + synchronize and the max over ranks is
+reported.
 """
 
 from __future__ import annotations
@@ -409,6 +412,108 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_sharded_arm(args, rank: int, world: int, dist) -> None:
+    """One B transform pair split over `world` GPUs (strong scaling)."""
+    import torch
+    from paper_1808_00896_b200.distributed import NativeShardBackend, ShardedSO3
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    b = args.bandwidth
+    n = 2 * b
+    C = coeff_count(b)
+    backend = NativeShardBackend(b, world, rank, device=dev)
+    sh = ShardedSO3(b, rank, world, backend)
+    m = sh.map
+    J = m.J
+    stream = torch.cuda.current_stream(dev)
+    host_c = seeded_coefficients(b, b)
+    coeffs = torch.from_numpy(host_c).to(dev)
+    # buffers reused across steps (the exchange is the only collective)
+    send_b = backend.empty(m.layout_b_rows(rank) * J)
+    recv_a = backend.empty(m.layout_a_rows() * J)
+    send_a = backend.empty(m.layout_a_rows() * J)
+    recv_b = backend.empty(m.layout_b_rows(rank) * J)
+    slab = backend.empty(n * J * n)
+    out = backend.zeros(C)
+
+    def step(evs=None):
+        rec = (lambda i: evs[i].record(stream)) if evs is not None else (lambda i: None)
+        rec(0)
+        backend.dwt_synthesis(coeffs, send_b)
+        rec(1)
+        sh._all_to_all(recv_a, send_b, m.inverse_recv_splits(rank), m.inverse_send_splits(rank))
+        rec(2)
+        backend.fft_synthesis(recv_a, slab)
+        rec(3)
+        backend.fft_analysis(slab, send_a)
+        rec(4)
+        sh._all_to_all(recv_b, send_a, m.forward_recv_splits(rank), m.forward_send_splits(rank))
+        rec(5)
+        backend.dwt_analysis(recv_b, out)
+        rec(6)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local).start() if rank == 0 else None
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    ms_total = t0.elapsed_time(t1)
+    clk = clocks.stop() if clocks else None
+    names = ["dwt_synthesis", "all_to_all_inverse", "fft_synthesis", "fft_analysis", "all_to_all_forward",
+             "dwt_analysis"]
+    stage_ms = {nm: statistics.mean(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps))
+                for i, nm in enumerate(names)}
+    if dist is not None:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    # parity: gathered coefficients of the measured step == seeded input (round trip)
+    full = sh.gather_coefficients(out.clone())
+    got = full.cpu().numpy()
+    diff = np.abs(got - host_c)
+    if rank != 0:
+        return
+    peaks = measured_peaks()
+    fl = dwt_flops(b) / world   # this rank's share of the DWT (cost-balanced)
+    dom = max(("dwt_analysis", "dwt_synthesis"), key=lambda k: stage_ms[k])
+    achieved = fl / (stage_ms[dom] * 1e-3) / 1e12
+    a2a_bytes = 16 * (m.layout_a_rows() - m.pairs[rank]) * J   # bytes this rank sends to peers, forward
+    line = {
+        "metric": metric_name(b), "value": 2.0 * 1000.0 / ms_step, "unit": "transforms/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(workload_config(b, world), parallelism=f"sharded x{world}: beta slabs (J={J}) + "
+                       "cluster groups, one all_to_all per direction"),
+        "stages_rank0_ms": stage_ms,
+        "roofline": {"kernel": f"{dom} (rank 0, DMMA)", "bound": "fp64", "achieved": achieved,
+                     "peak": peaks["fp64_tflops"], "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"],
+                     "traffic": None, "algorithmic": "8*B*C(B)/world flop per rank and direction"},
+        "all_to_all": {"bytes_per_rank_per_direction": a2a_bytes,
+                       "GBps_forward": a2a_bytes / (stage_ms["all_to_all_forward"] * 1e-3) / 1e9,
+                       "GBps_inverse": a2a_bytes / (stage_ms["all_to_all_inverse"] * 1e-3) / 1e9},
+        "cpu_baseline": None, "e2e": None, "gpu_launches": 6 * args.steps,
+        "clocks": clk,
+        "parity": {"roundtrip_max_abs": float(diff.max()),
+                   "roundtrip_max_rel_of_max": float(diff.max() / np.abs(host_c).max())},
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -417,6 +522,8 @@ def main() -> None:
     ap.add_argument("--bandwidth", "-B", type=int, default=DEFAULT_B)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--dwt-variant", choices=("mma", "mma2", "simt"), default="mma")
+    ap.add_argument("--mode", choices=("auto", "single", "sharded", "replicas"), default="auto",
+                    help="auto: single GPU at N=1, sharded (one transform over N GPUs) at N>1")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -438,7 +545,11 @@ def main() -> None:
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         tdist.init_process_group("nccl")
         dist = tdist
-    run_gpu_arm(args, rank, world, dist)
+    mode = args.mode if args.mode != "auto" else ("single" if world == 1 else "sharded")
+    if mode == "sharded":
+        run_sharded_arm(args, rank, world, dist)
+    else:
+        run_gpu_arm(args, rank, world, dist)
     if dist is not None:
         dist.destroy_process_group()
 

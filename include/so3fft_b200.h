@@ -137,6 +137,33 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */
 void* so3_plan_scratch(so3_plan_t plan);
 
+/* ---- sharded pipeline (one process per GPU) -------------------
+ * G ranks split the torus FFT by beta slab [rank*J, (rank+1)*J), J = 2B/G, and the DWT by
+ * cost-balanced cluster groups (longest-processing-time greedy over the schedule); one
+ * all-to-all per direction joins them (the reference's in-memory transpose spectrum[m, j, m'],
+ * soft.py:131-132, 142, 167).  Buffers (complex128):
+ *   slab     : [i][jj][k], 2B x J x 2B (this rank's samples; grid[:, jbase:jbase+J, :])
+ *   layout A : rows [rank g][pairs_g][J]   (forward send / inverse recv, total (2B-1)^2 * J)
+ *   layout B : rows [rank h][pairs_rank][J] (forward recv / inverse send, G * pairs_rank * J)
+ *   coeffs   : full l-major array; a rank writes (forward) / reads (inverse) only its slots.
+ * Results are identical, bit for bit, for every G (the same per-row FFTs and per-cluster
+ * reductions run whatever the split). */
+int so3_shard_plan_create(int bandwidth, int world, int rank, so3_plan_t* out);
+int64_t so3_shard_slab_width(so3_plan_t plan);             /* J */
+int64_t so3_shard_rank_pairs(so3_plan_t plan);             /* pairs_rank */
+/* host only: pairs per rank [world]; cluster owner per schedule entry; a rank's pairs (m, m') */
+int so3_shard_pair_counts(int bandwidth, int world, int64_t* pairs_per_rank);
+int so3_shard_cluster_owner(int bandwidth, int world, int32_t* owner);
+int so3_shard_pair_list(int bandwidth, int world, int rank, int32_t* pairs);
+/* forward: slab -> layout A (K1a + K1b with the pack fused into the store) */
+int so3_shard_fft_analysis(so3_plan_t plan, const void* slab_dev, void* send_dev, void* stream);
+/* forward: layout B -> this rank's coefficient slots */
+int so3_shard_dwt_analysis(so3_plan_t plan, const void* recv_dev, void* coeffs_dev, void* stream);
+/* inverse: this rank's coefficient slots -> layout B */
+int so3_shard_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* send_dev, void* stream);
+/* inverse: layout A -> slab (K4a with the unpack fused into the load, K4b) */
+int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_dev, void* stream);
+
 /* Wigner rows d^l_{m,m'}(beta_j), l = max(|m|,|m'|)..B-1, j < 2B, for any pair
  * (wigner_d_rows, wigner.py:139-178 + derive_cluster_matrices, dwt.py:76-93):
  * out_dev[(l-L)*2B + j], generated by the same in-register recurrence as the DWT. */

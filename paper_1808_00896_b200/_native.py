@@ -52,6 +52,16 @@ SIGNATURES = {
     "so3_plan_scratch": (_vp, [_vp]),
     "so3_plan_set_dwt_variant": (_c_int, [_vp, _c_int]),
     "so3_wigner_rows": (_c_int, [_vp, _c_int, _c_int, _vp, _vp]),
+    "so3_shard_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
+    "so3_shard_slab_width": (_c_i64, [_vp]),
+    "so3_shard_rank_pairs": (_c_i64, [_vp]),
+    "so3_shard_pair_counts": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_i64)]),
+    "so3_shard_cluster_owner": (_c_int, [_c_int, _c_int, _i32p]),
+    "so3_shard_pair_list": (_c_int, [_c_int, _c_int, _c_int, _i32p]),
+    "so3_shard_fft_analysis": (_c_int, [_vp, _vp, _vp, _vp]),
+    "so3_shard_dwt_analysis": (_c_int, [_vp, _vp, _vp, _vp]),
+    "so3_shard_dwt_synthesis": (_c_int, [_vp, _vp, _vp, _vp]),
+    "so3_shard_fft_synthesis": (_c_int, [_vp, _vp, _vp, _vp]),
 }
 
 

@@ -17,6 +17,12 @@ __device__ __forceinline__ long long coeff_slot(int l, int m, int mp) {
   return L * (4 * L * L - 1) / 3 + (long long)(m + l) * (2 * l + 1) + (mp + l);
 }
 
+// 32-bit form, valid while B(4B^2-1)/3 < 2^31 (B <= 812); the plan rejects larger B on
+// the paths that use it.
+__device__ __forceinline__ int coeff_slot32(int l, int m, int mp) {
+  return (l * (4 * l * l - 1)) / 3 + (m + l) * (2 * l + 1) + (mp + l);
+}
+
 // The eight symmetry relations of reference wigner.py:244-256, in tag order:
 // identity, negate_both, swap, swap_negate_both, negate_m, negate_mp,
 // swap_negate_m, swap_negate_mp.  Fields: reflect, sl, sm, smp, tm_m, tm_mp,

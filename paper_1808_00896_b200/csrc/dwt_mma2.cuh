@@ -1,49 +1,26 @@
-// DWT on the FP64 tensor path, software-pipelined and barrier-free in the main loop.
+// DWT on the FP64 tensor path, barrier-free main loops (variant SO3_DWT_MMA2).
 //
-// Same mathematics and fragment layouts as dwt_mma.cuh (reference dwt.py:109-125,
-// wigner.py:139-178).  What changes is the schedule, after ncu showed the FP64 pipe idle
-// ~45% of the time in the tile-synchronous kernels (profiles/): every warp ran its
-// latency-bound recurrence at the same moment after each CTA barrier.
+// Same mathematics and DMMA fragment layouts as dwt_mma.cuh (reference dwt.py:109-125,
+// wigner.py:139-178).  ncu on the tile-synchronous kernels showed the FP64 pipe idle ~35%
+// of the time in per-tile coefficient staging (+ CTA barrier) and, for the analysis, in
+// the barrier-synchronised reduction over warps.  Here no warp ever waits at a CTA
+// barrier inside the loop:
 //
-//  * Each warp overlaps the recurrence for the NEXT block of degrees (writing one half of
-//    a double-buffered Wigner tile Dt) with the DMMAs of the CURRENT block (reading the
-//    other half), so its own DFMA chain fills the issue gaps of its DMMA stream.
-//  * Synthesis: warps are independent.  Each warp stages its own copy of the signed
-//    coefficient tiles with cp.async (double buffered, no CTA barrier); recurrence
-//    coefficients come from the plan table, one tile per lane, broadcast by shuffles.
-//  * Analysis: the per-block partial sums (16 member rows x 8 degrees per warp) go into a
-//    ring of R shared slots guarded by mbarriers; block b is reduced by warp b % W while
-//    the other warps run ahead (at most R blocks), so no warp ever waits at a CTA barrier.
-//    The reduction order over warps is fixed, so results are bit-reproducible.
+//  * Each iteration issues the DMMAs of the current degree block FIRST and the
+//    recurrence for the NEXT block after them (double-buffered Wigner tile Dt, one
+//    __syncwarp per iteration), so the scheduler can hide the recurrence's DFMA chain in
+//    the issue gaps of the DMMA stream.  The padding member tile of 1/4-member clusters
+//    is computed anyway (0.6% extra work) so the loop body is a single basic block.
+//  * Synthesis: each lane loads its two B-fragment coefficients straight from global
+//    memory two quads ahead (sign applied at use); no shared staging at all.
+//  * Analysis: per-block partial sums go to a ring of R shared slots; the LAST warp to
+//    arrive at a slot (shared atomic counter) reduces it, so nobody waits for stragglers.
+//    Reduction order over warps is fixed, so results are bit-reproducible.
 #pragma once
 #include "common.cuh"
 #include "dwt.cuh"
 
 namespace so3 {
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool full) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(full ? 16 : 0)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ double flip_if(double v, int odd) {
   return __longlong_as_double(__double_as_longlong(v) ^ ((long long)(odd & 1) << 63));
@@ -68,23 +45,19 @@ __device__ __forceinline__ double3 rc_shfl(const double3& v, int src) {
 
 template <int JW>
 struct Mma2 {
-  static constexpr int S = JW + 4;      // Dt row stride (doubles): conflict-free STS and fragment LDS
-  static constexpr int CF = 10;         // coefficient-tile row stride (complex): conflict-free LDS
-  static constexpr int LT = 32;         // degrees per coefficient / recurrence-coefficient tile
-  // synthesis, per warp: Dt 8 rows + two coefficient tiles
-  static constexpr size_t syn_warp_doubles = (size_t)8 * S + 2 * LT * CF * 2;
-  // analysis, per warp: Dt 16 rows; ring: R slots x W warps x 128 doubles
-  static constexpr int R = 4;
-  static constexpr size_t ana_dt_doubles = (size_t)16 * S;
+  static constexpr int S = JW + 4;   // Dt row stride (doubles): conflict-free STS and fragment LDS
+  static constexpr int R = 4;        // analysis ring slots
+  static constexpr size_t syn_warp_doubles = (size_t)8 * S;     // two 4-row halves
+  static constexpr size_t ana_warp_doubles = (size_t)16 * S;    // two 8-row halves
 };
 
 // ------------------------------------------------------------------------------------------
-// synthesis  g(j, r) = sum_l d^l(beta_j) F(l, r)
+// synthesis  g(j, r) = sum_l d^l(beta_j) F(l, r); 4 warps per CTA, CTAs of a cluster independent
 // ------------------------------------------------------------------------------------------
-template <int JW>
-__global__ void __launch_bounds__(128, 2) dwt_synthesis_mma2_kernel(DwtArgs a, int split) {
+template <int JW, int MINB>
+__global__ void __launch_bounds__(128, MINB) dwt_synthesis_mma2_kernel(DwtArgs a, int split) {
   using K = Mma2<JW>;
-  constexpr int JT = JW / 32, MT = JW / 8, S = K::S, CF = K::CF, LT = K::LT;
+  constexpr int JT = JW / 32, MT = JW / 8, S = K::S;
   extern __shared__ double dsm[];
   __shared__ Member mem[8];
 
@@ -97,29 +70,29 @@ __global__ void __launch_bounds__(128, 2) dwt_synthesis_mma2_kernel(DwtArgs a, i
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int g = lane >> 2, tq = lane & 3;
   double2* spec = const_cast<double2*>(a.spec) + (long long)f * a.spec_fstride;
-  const double2* coef = a.coef + (long long)f * a.coef_fstride;
-  double* Dt = dsm + (size_t)warp * K::syn_warp_doubles;          // [2][4][S]
-  double2* cf = reinterpret_cast<double2*>(Dt + 8 * S);           // [2][LT][CF]
+  const double* coefd = reinterpret_cast<const double*>(a.coef + (long long)f * a.coef_fstride);
+  double* Dt = dsm + (size_t)warp * K::syn_warp_doubles;
 
-  if (t < 8) mem[t] = make_member(m, mp, t, n);
+  if (t < 8) mem[t] = member_of(a, m, mp, t);
   __syncthreads();
-  const bool two_tiles = mem[4].valid;
-  const int nsteps = B - 1 - m;       // recurrence steps l -> l+1 of this cluster
-  const int nq = (B - m + 3) >> 2;    // quads of degrees
+  const int nsteps = B - 1 - m;
+  const int nq = (B - m + 3) >> 2;
   const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
 
-  // coefficient tile T (degrees m + 32T ..) -> cf[T & 1] via cp.async (zero-filled past B)
-  auto stage = [&](int T) {
-    double2* dst = cf + (T & 1) * LT * CF;
-#pragma unroll
-    for (int i = 0; i < LT * 8 / 32; ++i) {
-      const int idx = lane + 32 * i, ll = idx >> 3, k = idx & 7;
-      const int l = m + LT * T + ll;
-      const Member& M = mem[k];
-      const bool ok = l < B && M.valid;
-      cp_async16(&dst[ll * CF + k], ok ? &coef[coeff_slot(l, M.pm, M.pmp)] : coef, ok);
-    }
-    cp_async_commit();
+  // B-fragment coefficients of this lane: F(l, r) for r = g (member g>>1) and 8+g (4+(g>>1))
+  const Member M0 = mem[g >> 1], M1 = mem[4 + (g >> 1)];
+  const int comp = g & 1;
+  // branch-free: out-of-range lanes load slot 0 and are zeroed
+  auto fetch = [&](int Q, double& f0, double& f1) {
+    const int l = m + 4 * Q + tq;
+    const bool ok0 = l < B && M0.valid, ok1 = l < B && M1.valid;
+    const int lc = ok0 || ok1 ? l : 0;
+    const int s0 = ok0 ? coeff_slot32(lc, M0.pm, M0.pmp) : 0;
+    const int s1 = ok1 ? coeff_slot32(lc, M1.pm, M1.pmp) : 0;
+    const double v0 = __ldg(&coefd[2 * s0 + comp]);
+    const double v1 = __ldg(&coefd[2 * s1 + comp]);
+    f0 = ok0 ? v0 : 0.0;
+    f1 = ok1 ? v1 : 0.0;
   };
 
   const int jw0 = (crank * 4 + warp) * JW;
@@ -139,21 +112,16 @@ __global__ void __launch_bounds__(128, 2) dwt_synthesis_mma2_kernel(DwtArgs a, i
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) acc[i][nt][0] = acc[i][nt][1] = 0.0;
 
-  // the member / component this lane feeds into the B fragments (F(l, r) for r = g, 8 + g)
-  const Member M0 = mem[g >> 1], M1 = mem[4 + (g >> 1)];
-  const int comp = g & 1;
-
-  // recurrence for quad Q into Dt half (Q & 1); rcw holds steps 32*(Q/8) .. of this lane's tile
+  // 4 degrees of the base column into Dt half (Q & 1); steps past the cluster's last degree
+  // have zero coefficients, so those rows come out exactly zero.
   auto recur = [&](int Q, const double3& rcw) {
     double* D = Dt + (Q & 1) * 4 * S;
 #pragma unroll
     for (int ll = 0; ll < 4; ++ll) {
-      const int s = 4 * Q + ll;                       // step index l - m
-      const double3 k3 = rc_shfl(rcw, s & (LT - 1));
-      const bool live = s < B - m;
+      const double3 k3 = rc_shfl(rcw, (4 * Q + ll) & 31);
 #pragma unroll
       for (int q = 0; q < JT; ++q) {
-        D[ll * S + lane + 32 * q] = live ? cur[q] : 0.0;
+        D[ll * S + lane + 32 * q] = cur[q];
         const double tt = fma(k3.x, x[q], -k3.y);
         const double nx = fma(tt, cur[q], -k3.z * prev[q]);
         prev[q] = cur[q];
@@ -162,47 +130,36 @@ __global__ void __launch_bounds__(128, 2) dwt_synthesis_mma2_kernel(DwtArgs a, i
     }
   };
 
-  stage(0);
-  if (nq > 8) stage(1); else cp_async_commit();
   double3 rc_cur = rc_load(rct, 0, lane, nsteps);
-  double3 rc_nxt = rc_load(rct, LT, lane, nsteps);
+  double3 rc_nxt = rc_load(rct, 32, lane, nsteps);
+  double fa0, fa1, fb0, fb1;
+  fetch(0, fa0, fa1);
+  fetch(1, fb0, fb1);
   recur(0, rc_cur);
-  cp_async_wait<1>();
   __syncwarp();
   for (int Q = 0; Q < nq; ++Q) {
-    const int T = Q >> 3, qi = Q & 7;
-    // (A) next quad's Wigner rows (other Dt half), overlapped with (B)
-    if (Q + 1 < nq) recur(Q + 1, qi == 7 ? rc_nxt : rc_cur);
-    // (B) this quad's DMMAs
+    // (1) DMMAs of quad Q (Dt half Q & 1)
     {
-      const double* D = Dt + (Q & 1) * 4 * S;
-      const double2* F = cf + (T & 1) * LT * CF + (4 * qi + tq) * CF;
       const int l = m + 4 * Q + tq;
-      const double2 f0 = F[g >> 1], f1 = F[4 + (g >> 1)];
-      const double b0 = flip_if(comp ? f0.y : f0.x, M0.sl * l + M0.par0);
-      const double b1 = flip_if(comp ? f1.y : f1.x, M1.sl * l + M1.par0);
-      if (two_tiles) {
+      const double b0 = flip_if(fa0, M0.sl * l + M0.par0);
+      const double b1 = flip_if(fa1, M1.sl * l + M1.par0);
+      const double* D = Dt + (Q & 1) * 4 * S;
 #pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const double av = D[tq * S + 8 * i + g];
-          dmma_884(acc[i][0][0], acc[i][0][1], av, b0);
-          dmma_884(acc[i][1][0], acc[i][1][1], av, b1);
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < MT; ++i) {
-          const double av = D[tq * S + 8 * i + g];
-          dmma_884(acc[i][0][0], acc[i][0][1], av, b0);
-        }
+      for (int i = 0; i < MT; ++i) {
+        const double av = D[tq * S + 8 * i + g];
+        dmma_884(acc[i][0][0], acc[i][0][1], av, b0);
+        dmma_884(acc[i][1][0], acc[i][1][1], av, b1);
       }
     }
-    if (qi == 7) {   // tile T done: its coefficient buffer is free for tile T + 2
+    // (2) prefetch quad Q+2's coefficients, recurrence for quad Q+1 (other Dt half)
+    fa0 = fb0;
+    fa1 = fb1;
+    fetch(Q + 2, fb0, fb1);
+    if (((Q + 1) & 7) == 0) {   // the next quad starts a new 32-step window
       rc_cur = rc_nxt;
-      rc_nxt = rc_load(rct, LT * (T + 2), lane, nsteps);
-      __syncwarp();
-      if (8 * (T + 2) < nq) stage(T + 2); else cp_async_commit();
-      cp_async_wait<1>();   // tile T + 1 has landed
+      rc_nxt = rc_load(rct, 4 * (Q + 1) + 32, lane, nsteps);
     }
+    recur(Q + 1, rc_cur);
     __syncwarp();
   }
   // lane (g, tq) holds g(j = jw0 + 8 i + g, member 4 nt + tq) as (re, im)
@@ -213,21 +170,22 @@ __global__ void __launch_bounds__(128, 2) dwt_synthesis_mma2_kernel(DwtArgs a, i
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       const Member M = mem[4 * nt + tq];
-      if (M.valid) spec[M.row * n + (M.reflect ? n - 1 - j : j)] = make_double2(acc[i][nt][0], acc[i][nt][1]);
+      if (M.valid) spec[spec_index(a, M.row, M.reflect ? n - 1 - j : j)] = make_double2(acc[i][nt][0], acc[i][nt][1]);
     }
   }
 }
 
 // ------------------------------------------------------------------------------------------
-// analysis  out(r, l) = sum_j x'_r(j) d^l(beta_j)
+// analysis  out(r, l) = sum_j x'_r(j) d^l(beta_j); one CTA (W warps) per cluster
 // ------------------------------------------------------------------------------------------
 template <int JW>
 __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
   using K = Mma2<JW>;
-  constexpr int JT = JW / 32, KS = JW / 4, S = K::S, LT = K::LT, R = K::R;
+  constexpr int JT = JW / 32, KS = JW / 4, S = K::S, R = K::R;
   extern __shared__ double dsm[];
   __shared__ Member mem[8];
-  __shared__ unsigned long long full_bar[R], empty_bar[R];
+  __shared__ int arrive[R];
+  __shared__ volatile int slot_free[R];   // first block index allowed to use the slot
 
   const int c = a.cluster0 + blockIdx.x;
   const int f = blockIdx.y;
@@ -238,18 +196,16 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
   const int g = lane >> 2, tq = lane & 3;
   const double2* spec = a.spec + (long long)f * a.spec_fstride;
   double2* coef = a.coef + (long long)f * a.coef_fstride;
-  double* Dt = dsm + (size_t)warp * K::ana_dt_doubles;         // [2][8][S]
-  double* ring = dsm + (size_t)W * K::ana_dt_doubles;          // [R][W][128]
+  double* Dt = dsm + (size_t)warp * K::ana_warp_doubles;   // [2][8][S]
+  double* ring = dsm + (size_t)W * K::ana_warp_doubles;    // [R][W][128]
 
-  if (t < 8) mem[t] = make_member(m, mp, t, n);
-  if (t < R) { mbar_init(&full_bar[t], W); mbar_init(&empty_bar[t], 1); }
+  if (t < 8) mem[t] = member_of(a, m, mp, t);
+  if (t < R) { arrive[t] = 0; slot_free[t] = t; }
   __syncthreads();
-  const bool two_tiles = mem[4].valid;
   const int nsteps = B - 1 - m;
-  const int nb = (B - m + 7) >> 3;    // blocks of 8 degrees
+  const int nb = (B - m + 7) >> 3;   // blocks of 8 degrees
   const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
 
-  // A fragments: x'_r(j), r = 8 mt + g, j = jw0 + 4 s + tq (loaded once)
   const int jw0 = warp * JW;
   double afr[KS][2];
 #pragma unroll
@@ -261,7 +217,7 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
       const Member M = mem[r >> 1];
       double v = 0.0;
       if (j < n && M.valid) {
-        const double* e = reinterpret_cast<const double*>(&spec[M.row * n + (M.reflect ? n - 1 - j : j)]);
+        const double* e = reinterpret_cast<const double*>(&spec[spec_index(a, M.row, M.reflect ? n - 1 - j : j)]);
         v = e[r & 1];
       }
       afr[s][mt] = v;
@@ -277,17 +233,14 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
     cur[q] = ok ? seed_value(m, mp, ln, a.logcs[j]) : 0.0;
     prev[q] = 0.0;
   }
-
   auto recur = [&](int b, const double3& rcw) {
     double* D = Dt + (b & 1) * 8 * S;
 #pragma unroll
     for (int ll = 0; ll < 8; ++ll) {
-      const int s = 8 * b + ll;
-      const double3 k3 = rc_shfl(rcw, s & (LT - 1));
-      const bool live = s < B - m;
+      const double3 k3 = rc_shfl(rcw, (8 * b + ll) & 31);
 #pragma unroll
       for (int q = 0; q < JT; ++q) {
-        D[ll * S + lane + 32 * q] = live ? cur[q] : 0.0;
+        D[ll * S + lane + 32 * q] = cur[q];
         const double tt = fma(k3.x, x[q], -k3.y);
         const double nx = fma(tt, cur[q], -k3.z * prev[q]);
         prev[q] = cur[q];
@@ -298,47 +251,44 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
 
   const double vscale = 8.0 * 3.141592653589793 * (double)B;
   double3 rc_cur = rc_load(rct, 0, lane, nsteps);
-  double3 rc_nxt = rc_load(rct, LT, lane, nsteps);
+  double3 rc_nxt = rc_load(rct, 32, lane, nsteps);
   recur(0, rc_cur);
   __syncwarp();
   for (int b = 0; b < nb; ++b) {
-    const int T = b >> 2, bi = b & 3;
-    if (b + 1 < nb) recur(b + 1, bi == 3 ? rc_nxt : rc_cur);
+    // (1) DMMAs of block b
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
     {
       const double* D = Dt + (b & 1) * 8 * S;
-      if (two_tiles) {
 #pragma unroll
-        for (int s = 0; s < KS; ++s) {
-          const double bv = D[g * S + 4 * s + tq];
-          dmma_884(acc[0][0], acc[0][1], afr[s][0], bv);
-          dmma_884(acc[1][0], acc[1][1], afr[s][1], bv);
-        }
-      } else {
-#pragma unroll
-        for (int s = 0; s < KS; ++s) {
-          const double bv = D[g * S + 4 * s + tq];
-          dmma_884(acc[0][0], acc[0][1], afr[s][0], bv);
-        }
+      for (int s = 0; s < KS; ++s) {
+        const double bv = D[g * S + 4 * s + tq];
+        dmma_884(acc[0][0], acc[0][1], afr[s][0], bv);
+        dmma_884(acc[1][0], acc[1][1], afr[s][1], bv);
       }
     }
-    if (bi == 3) {
+    // (2) recurrence for block b+1 into the other Dt half
+    if (((b + 1) & 3) == 0) {
       rc_cur = rc_nxt;
-      rc_nxt = rc_load(rct, LT * (T + 2), lane, nsteps);
+      rc_nxt = rc_load(rct, 8 * (b + 1) + 32, lane, nsteps);
     }
-    __syncwarp();   // Dt half (b & 1) is free for block b + 2
-    // publish this warp's partials C[r = 8 mt + g][l = 8 b + 2 tq + e]
+    recur(b + 1, rc_cur);
+    // (3) publish partials C[r = 8 mt + g][l = 8 b + 2 tq + e]; the last warp to arrive reduces
     const int slot = b % R;
-    if (b >= R) mbar_wait(&empty_bar[slot], ((b / R) - 1) & 1);
+    if (lane == 0) { while (slot_free[slot] < b) { } }
+    __syncwarp();
     double* pw = ring + ((size_t)slot * W + warp) * 128;
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
       *reinterpret_cast<double2*>(pw + (mt * 32 + lane) * 2) = make_double2(acc[mt][0], acc[mt][1]);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&full_bar[slot]);
-    // rotating reducer: warp b % W finishes block b
-    if (b % W == warp) {
-      mbar_wait(&full_bar[slot], (b / R) & 1);
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = (atomicAdd(&arrive[slot], 1) == W - 1);
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      __threadfence_block();
       const double* ps = ring + (size_t)slot * W * 128;
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
@@ -357,12 +307,17 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
           }
           double sc = (2.0 * l + 1.0) / vscale;
           if ((M.sl * l + M.par0) & 1) sc = -sc;
-          coef[coeff_slot(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
+          coef[coeff_slot32(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+      if (lane == 0) {
+        arrive[slot] = 0;
+        __threadfence_block();
+        slot_free[slot] = b + R;
+      }
     }
+    __syncwarp();
   }
 }
 

@@ -39,6 +39,11 @@ struct FftArgs {
   long long fs_out, sy_out, sx_out, sp_out;
   const double2* tw;          // N entries, exp(+2 pi i k / N)
   const double* w;            // quadrature weights
+  // sharded passes: the pair-major side is addressed through a row table instead of strides,
+  // element (x, y, p) at base + tab[y*N + p] * tabJ + x (tab < 0: not stored / read as zero)
+  const int* tab_in;
+  const int* tab_out;
+  int tabJ;
 };
 
 // exp(SIGN * 2 pi i * Q / 16) * a, Q compile-time
@@ -214,23 +219,39 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
   double2* row = smem + xl * RowLayout<N, XB>::SIZE;
 
   double2 v[16];
+  if (a.tab_in) {
+    const double2* base = a.src + f * a.fs_in + x;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const int p = t + e * TPR;
-    const bool zero = !xvalid || p == a.zero_p;
-    v[e] = zero ? make_double2(0.0, 0.0) : src[(long long)p * a.sp_in];
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      const int r = (xvalid && p != a.zero_p) ? __ldg(&a.tab_in[(long long)y * N + p]) : -1;
+      v[e] = r >= 0 ? base[(long long)r * a.tabJ] : make_double2(0.0, 0.0);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      const bool zero = !xvalid || p == a.zero_p;
+      v[e] = zero ? make_double2(0.0, 0.0) : src[(long long)p * a.sp_in];
+    }
   }
   fft_rows<N, SIGN>(v, t, a.tw, row);
   double wx = 1.0;
   if (a.weight && xvalid) wx = __ldg(&a.w[a.jbase + x]);
   if (xvalid) {
+    double2* tbase = a.dst + f * a.fs_out + x;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       const int p = t + e * TPR;
       double2 z = v[e];
       z.x *= wx;
       z.y *= wx;
-      dst[(long long)p * a.sp_out] = z;
+      if (a.tab_out) {
+        const int r = __ldg(&a.tab_out[(long long)y * N + p]);
+        if (r >= 0) tbase[(long long)r * a.tabJ] = z;
+      } else {
+        dst[(long long)p * a.sp_out] = z;
+      }
     }
   }
 }
@@ -251,7 +272,12 @@ __global__ void __launch_bounds__(256) dft_direct_kernel(FftArgs a, int XC) {
   for (int idx = threadIdx.x; idx < xc * n; idx += blockDim.x) {
     const int xl = idx % xc, p = idx / xc;
     double2 z = make_double2(0.0, 0.0);
-    if (p != a.zero_p) z = src[(long long)(x0 + xl) * a.sx_in + (long long)p * a.sp_in];
+    if (a.tab_in) {
+      const int r = p != a.zero_p ? a.tab_in[(long long)y * n + p] : -1;
+      if (r >= 0) z = a.src[f * a.fs_in + (long long)r * a.tabJ + x0 + xl];
+    } else if (p != a.zero_p) {
+      z = src[(long long)(x0 + xl) * a.sx_in + (long long)p * a.sp_in];
+    }
     col[p * XC + xl] = z;
   }
   __syncthreads();
@@ -264,7 +290,12 @@ __global__ void __launch_bounds__(256) dft_direct_kernel(FftArgs a, int XC) {
       acc = cadd(acc, cmul(col[p * XC + xl], w));
     }
     if (a.weight) { const double wx = a.w[a.jbase + x0 + xl]; acc.x *= wx; acc.y *= wx; }
-    dst[(long long)(x0 + xl) * a.sx_out + (long long)q * a.sp_out] = acc;
+    if (a.tab_out) {
+      const int r = a.tab_out[(long long)y * n + q];
+      if (r >= 0) a.dst[f * a.fs_out + (long long)r * a.tabJ + x0 + xl] = acc;
+    } else {
+      dst[(long long)(x0 + xl) * a.sx_out + (long long)q * a.sp_out] = acc;
+    }
   }
 }
 

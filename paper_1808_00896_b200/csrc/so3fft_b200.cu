@@ -78,6 +78,36 @@ std::vector<Cluster> host_clusters(int b) {
   return cl;
 }
 
+// Cost-balanced cluster groups for `world` ranks: longest-processing-time greedy over the
+// cost-sorted schedule (cost = members * (B - m), the DWT work of a cluster).  The GPU form
+// of the reference's dynamic work split (schedule.py:200-248) across devices.
+std::vector<int> shard_owner(const std::vector<Cluster>& cl, int b, int world) {
+  std::vector<long long> load(world, 0);
+  std::vector<int> owner(cl.size());
+  for (size_t i = 0; i < cl.size(); ++i) {
+    int best = 0;
+    for (int r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    owner[i] = best;
+    load[best] += (long long)cl[i].members * (b - cl[i].m) + 1;
+  }
+  return owner;
+}
+
+// Member order pairs of a base pair in tag order (schedule.py:115-133), as make_member.
+std::vector<std::pair<int, int>> cluster_pairs(int m, int mp) {
+  static const int rel[8][4] = {{1, 0, 0, 1}, {-1, 0, 0, -1}, {0, 1, 1, 0}, {0, -1, -1, 0},
+                                {-1, 0, 0, 1}, {1, 0, 0, -1}, {0, -1, 1, 0}, {0, 1, -1, 0}};
+  std::vector<int> tags;
+  if (m == 0) tags = {0};
+  else if (mp == 0) tags = {0, 1, 2, 3};
+  else if (mp == m) tags = {0, 1, 4, 5};
+  else tags = {0, 1, 2, 3, 4, 5, 6, 7};
+  std::vector<std::pair<int, int>> out;
+  for (int t : tags) out.push_back({rel[t][0] * m + rel[t][1] * mp, rel[t][2] * m + rel[t][3] * mp});
+  return out;
+}
+
 void split_ld(long double v, double* hi, double* lo) {
   *hi = (double)v;
   *lo = (double)(v - (long double)*hi);
@@ -102,6 +132,12 @@ struct so3_plan_s {
   double2* d_grid_stage = nullptr;
   double2* d_coef_stage = nullptr;
   int64_t bytes = 0;
+  // sharding (world > 1 or a sharded plan): beta slab [jbase, jbase + J) and a cluster group
+  int sharded = 0, world = 1, rank = 0, J = 0, jbase = 0;
+  int64_t pairs_rank = 0;               // order pairs owned by this rank (DWT rows)
+  std::vector<int64_t> pairs_of;        // pairs per rank
+  int* d_row_global = nullptr;          // (m' bin)*n + (m bin) -> row of layout [rank g][pairs_g][J], -1 if none
+  int* d_row_local = nullptr;           // same index -> row among this rank's pairs, -1 if not owned
   int dwt_variant = SO3_DWT_MMA;
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
@@ -176,6 +212,8 @@ so3::FftArgs fft_pass_args(const so3_plan_s* p, int pass, const void* src, void*
   a.fs_in = a.fs_out = p->ngrid;
   a.tw = p->d_tw;
   a.w = p->d_w;
+  a.tab_in = a.tab_out = nullptr;
+  a.tabJ = 0;
   switch (pass) {
     case 0:   // K1a: grid[i][j][k] (x=i, y=j, p=k) -> T[j][m'][i]
       a.sx_in = n2; a.sy_in = n; a.sp_in = 1;
@@ -197,6 +235,38 @@ so3::FftArgs fft_pass_args(const so3_plan_s* p, int pass, const void* src, void*
       a.sx_in = 1; a.sy_in = n2; a.sp_in = n;
       a.sx_out = n2; a.sy_out = n; a.sp_out = 1;
       a.zero_p = p->B;
+      break;
+  }
+  return a;
+}
+
+// Sharded passes on a beta slab [jbase, jbase + J): the pair-major side is the all-to-all
+// buffer, rows [rank g][pairs_g][J] addressed through the global row table (fused pack/unpack).
+so3::FftArgs shard_pass_args(const so3_plan_s* p, int pass, const void* src, void* dst) {
+  const long long n = p->n, n2 = n * n, J = p->J;
+  so3::FftArgs a = fft_pass_args(p, pass, src, dst);
+  a.fs_in = a.fs_out = 0;
+  a.jbase = p->jbase;
+  switch (pass) {
+    case 0:   // K1a: slab[i][jj][k] (x=i, y=jj, p=k) -> T[jj][m'][i]
+      a.X = p->n; a.Y = p->J;
+      a.sx_in = J * n; a.sy_in = n; a.sp_in = 1;
+      a.sx_out = 1; a.sy_out = n2; a.sp_out = n;
+      break;
+    case 1:   // K1b: T[jj][m'][i] (x=jj, y=m', p=i) -> send rows [g][pairs_g][J] * w_j
+      a.X = p->J; a.Y = p->n;
+      a.sx_in = n2; a.sy_in = n; a.sp_in = 1;
+      a.tab_out = p->d_row_global; a.tabJ = p->J;
+      break;
+    case 2:   // K4a: recv rows (x=jj, y=m', p=m) -> T[jj][m'][i]
+      a.X = p->J; a.Y = p->n;
+      a.tab_in = p->d_row_global; a.tabJ = p->J;
+      a.sx_out = n2; a.sy_out = n; a.sp_out = 1;
+      break;
+    default:  // K4b: T[jj][m'][i] (x=i, y=jj, p=m') -> slab[i][jj][k]
+      a.X = p->n; a.Y = p->J;
+      a.sx_in = 1; a.sy_in = n2; a.sp_in = n;
+      a.sx_out = J * n; a.sy_out = n; a.sp_out = 1;
       break;
   }
   return a;
@@ -261,14 +331,14 @@ int launch_dwt_mma2(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, i
   const int warps = (n + JW - 1) / JW;
   if (analysis) {
     if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA2 analysis kernel");
-    const size_t smem = ((size_t)warps * K::ana_dt_doubles + (size_t)K::R * warps * 128) * sizeof(double);
+    const size_t smem = ((size_t)warps * K::ana_warp_doubles + (size_t)K::R * warps * 128) * sizeof(double);
     auto k = so3::dwt_analysis_mma2_kernel<JW>;
     SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<dim3(ncl, batch), warps * 32, smem, st>>>(a);
   } else {
     const int split = (warps + 3) / 4;
     const size_t smem = 4 * K::syn_warp_doubles * sizeof(double);
-    auto k = so3::dwt_synthesis_mma2_kernel<JW>;
+    auto k = so3::dwt_synthesis_mma2_kernel<JW, (JW >= 128 ? 2 : 4)>;
     SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     k<<<dim3(ncl * split, batch), 128, smem, st>>>(a, split);
   }
@@ -296,8 +366,11 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.cluster0 = (int)c0;
   a.rc = p->d_rc;
   a.rc_off = p->d_rc_off;
+  a.rowtab = p->sharded ? p->d_row_local : nullptr;
+  a.J = p->sharded ? p->J : p->n;
+  a.slab_stride = p->sharded ? (long long)p->pairs_rank * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
-  if (p->dwt_variant == SO3_DWT_MMA2 && p->n <= 1024) {
+  if (p->dwt_variant == SO3_DWT_MMA2 && p->n <= 1024 && p->B <= 812) {
     const int jw = ANALYSIS ? (p->n >= 1024 ? 128 : p->n >= 512 ? 64 : 32)
                             : (p->n >= 512 ? 128 : p->n >= 256 ? 64 : 32);
     switch (jw) {
@@ -400,24 +473,13 @@ int so3_cluster_schedule(int b, int32_t* bases, int32_t* members) {
   return SO3_OK;
 }
 
-int so3_plan_create(int b, int batch, so3_plan_t* out) {
-  if (!out) return fail(SO3_ERR_INVALID, "null plan output");
-  *out = nullptr;
-  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
-  if (batch < 1) return fail(SO3_ERR_INVALID, "batch must be >= 1, got " + std::to_string(batch));
-  if (b > 1024) return fail(SO3_ERR_INVALID, "bandwidth > 1024 does not fit one device");
-  auto* p = new so3_plan_s();
-  p->B = b;
-  p->n = 2 * b;
-  p->batch = batch;
-  p->ncoef = so3_coeff_count(b);
-  p->ngrid = so3_grid_count(b);
-  cudaGetDevice(&p->device);
-  if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
-  if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
-  if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
-  const int n = p->n;
+}  // extern "C"
 
+namespace {
+
+// Tables and buffers of a plan over the cluster list `cl` (all clusters, or one rank's group).
+int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
+  const int b = p->B, n = p->n, batch = p->batch;
   std::vector<double> w(n), cosb(n);
   std::vector<double4> logcs(n);
   std::vector<double2> tw(n);
@@ -434,16 +496,17 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
     const long double th = 2.0L * kPi * k / n;
     tw[k] = make_double2((double)cosl(th), (double)sinl(th));
   }
-  const auto cl = host_clusters(b);
   p->nclusters = (int64_t)cl.size();
-  std::vector<long long> rc_off(cl.size());
+  const size_t ncl = std::max<size_t>(cl.size(), 1);
+  std::vector<long long> rc_off(ncl, 0);
   long long rc_entries = 0;
   for (size_t i = 0; i < cl.size(); ++i) {
     rc_off[i] = rc_entries;
     rc_entries += std::max(1, b - 1 - cl[i].m);
   }
-  std::vector<int2> bases(cl.size());
-  std::vector<double2> lnorm(cl.size());
+  rc_entries = std::max(rc_entries, 1LL);
+  std::vector<int2> bases(ncl, make_int2(0, 0));
+  std::vector<double2> lnorm(ncl, make_double2(0.0, 0.0));
   for (size_t i = 0; i < cl.size(); ++i) {
     const int m = cl[i].m, mp = cl[i].mp;
     bases[i] = make_int2(m, mp);
@@ -453,44 +516,160 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
     split_ld(ln, &hi, &lo);
     lnorm[i] = make_double2(hi, lo);
   }
+  // slab size of the spectrum buffers: whole grid, or this rank's pair rows x 2B
+  const size_t spec_elems = p->sharded ? (size_t)std::max<int64_t>(p->pairs_rank, 1) * n : (size_t)p->ngrid;
+  const size_t slab_elems = p->sharded ? (size_t)n * p->J * n : (size_t)p->ngrid;
 
-  auto cleanup = [p]() { so3_plan_destroy(p); };
 #define PLAN_ALLOC(ptr, count)                                                                    \
   do {                                                                                            \
     size_t _bytes = (size_t)(count) * sizeof(*(ptr));                                             \
     cudaError_t _e = cudaMalloc((void**)&(ptr), _bytes);                                          \
-    if (_e != cudaSuccess) { cleanup(); return fail(SO3_ERR_NOMEM, std::string("cudaMalloc(") +  \
-                                 std::to_string(_bytes) + "): " + cudaGetErrorString(_e)); }      \
+    if (_e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("cudaMalloc(") +               \
+                                 std::to_string(_bytes) + "): " + cudaGetErrorString(_e));        \
     p->bytes += (int64_t)_bytes;                                                                  \
   } while (0)
-  PLAN_ALLOC(p->d_bases, cl.size());
-  PLAN_ALLOC(p->d_lnorm, cl.size());
+  PLAN_ALLOC(p->d_bases, ncl);
+  PLAN_ALLOC(p->d_lnorm, ncl);
   PLAN_ALLOC(p->d_cosb, n);
   PLAN_ALLOC(p->d_logcs, n);
   PLAN_ALLOC(p->d_w, n);
   PLAN_ALLOC(p->d_tw, n);
-  PLAN_ALLOC(p->d_scratch, (size_t)p->ngrid * batch);
-  PLAN_ALLOC(p->d_spec, (size_t)p->ngrid * batch);
+  PLAN_ALLOC(p->d_scratch, slab_elems * batch);
+  PLAN_ALLOC(p->d_spec, spec_elems * batch);
   PLAN_ALLOC(p->d_rc, (size_t)3 * rc_entries);
-  PLAN_ALLOC(p->d_rc_off, cl.size());
+  PLAN_ALLOC(p->d_rc_off, ncl);
 #undef PLAN_ALLOC
   cudaError_t e = cudaSuccess;
-  e = e ? e : cudaMemcpy(p->d_bases, bases.data(), bases.size() * sizeof(int2), cudaMemcpyHostToDevice);
-  e = e ? e : cudaMemcpy(p->d_lnorm, lnorm.data(), lnorm.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_bases, bases.data(), ncl * sizeof(int2), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_lnorm, lnorm.data(), ncl * sizeof(double2), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_cosb, cosb.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_logcs, logcs.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
-  e = e ? e : cudaMemcpy(p->d_rc_off, rc_off.data(), rc_off.size() * sizeof(long long), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) {
+  e = e ? e : cudaMemcpy(p->d_rc_off, rc_off.data(), ncl * sizeof(long long), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !cl.empty()) {
     so3::rc_table_kernel<<<(unsigned)cl.size(), 128>>>(b, (int)cl.size(), p->d_bases, p->d_rc_off, p->d_rc);
     e = cudaGetLastError();
   }
   e = e ? e : cudaDeviceSynchronize();
-  if (e != cudaSuccess) { cleanup(); return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e)); }
+  if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  return SO3_OK;
+}
+
+so3_plan_s* new_plan(int b, int batch) {
+  auto* p = new so3_plan_s();
+  p->B = b;
+  p->n = 2 * b;
+  p->batch = batch;
+  p->ncoef = so3_coeff_count(b);
+  p->ngrid = so3_grid_count(b);
+  p->J = p->n;
+  cudaGetDevice(&p->device);
+  if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
+  if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
+  if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+int so3_plan_create(int b, int batch, so3_plan_t* out) {
+  if (!out) return fail(SO3_ERR_INVALID, "null plan output");
+  *out = nullptr;
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  if (batch < 1) return fail(SO3_ERR_INVALID, "batch must be >= 1, got " + std::to_string(batch));
+  if (b > 1024) return fail(SO3_ERR_INVALID, "bandwidth > 1024 does not fit one device");
+  so3_plan_s* p = new_plan(b, batch);
+  const int rc = build_plan(p, host_clusters(b));
+  if (rc) { so3_plan_destroy(p); return rc; }
   *out = p;
   return SO3_OK;
 }
+
+int so3_shard_plan_create(int b, int world, int rank, so3_plan_t* out) {
+  if (!out) return fail(SO3_ERR_INVALID, "null plan output");
+  *out = nullptr;
+  if (!valid_bandwidth(b) || b > 1024) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 1024], got " + std::to_string(b));
+  if (world < 1 || rank < 0 || rank >= world) return fail(SO3_ERR_INVALID, "rank outside [0, world)");
+  if ((2 * b) % world) return fail(SO3_ERR_INVALID, "2B must be divisible by the number of ranks");
+  so3_plan_s* p = new_plan(b, 1);
+  p->sharded = 1;
+  p->world = world;
+  p->rank = rank;
+  p->J = p->n / world;
+  p->jbase = rank * p->J;
+  const int n = p->n;
+  const auto all = host_clusters(b);
+  const auto owner = shard_owner(all, b, world);
+  std::vector<Cluster> mine;
+  p->pairs_of.assign(world, 0);
+  std::vector<int> row_global((size_t)n * n, -1), row_local((size_t)n * n, -1);
+  std::vector<int64_t> prefix(world + 1, 0);
+  for (size_t i = 0; i < all.size(); ++i) p->pairs_of[owner[i]] += all[i].members;
+  for (int r = 0; r < world; ++r) prefix[r + 1] = prefix[r] + p->pairs_of[r];
+  std::vector<int64_t> next(world, 0);
+  for (size_t i = 0; i < all.size(); ++i) {
+    const int r = owner[i];
+    if (r == rank) mine.push_back(all[i]);
+    for (const auto& pr : cluster_pairs(all[i].m, all[i].mp)) {
+      const int bm = ((pr.first % n) + n) % n, bmp = ((pr.second % n) + n) % n;
+      const size_t idx = (size_t)bmp * n + bm;
+      row_global[idx] = (int)(prefix[r] + next[r]);
+      if (r == rank) row_local[idx] = (int)next[r];
+      ++next[r];
+    }
+  }
+  p->pairs_rank = p->pairs_of[rank];
+  int rc = build_plan(p, mine);
+  if (rc) { so3_plan_destroy(p); return rc; }
+  cudaError_t e = cudaMalloc((void**)&p->d_row_global, row_global.size() * sizeof(int));
+  e = e ? e : cudaMalloc((void**)&p->d_row_local, row_local.size() * sizeof(int));
+  e = e ? e : cudaMemcpy(p->d_row_global, row_global.data(), row_global.size() * sizeof(int), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_row_local, row_local.data(), row_local.size() * sizeof(int), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { so3_plan_destroy(p); return fail(SO3_ERR_NOMEM, std::string("shard tables: ") + cudaGetErrorString(e)); }
+  p->bytes += (int64_t)(2 * row_global.size() * sizeof(int));
+  *out = p;
+  return SO3_OK;
+}
+
+int so3_shard_pair_counts(int b, int world, int64_t* pairs_per_rank) {
+  if (!valid_bandwidth(b) || world < 1 || !pairs_per_rank) return fail(SO3_ERR_INVALID, "bad arguments");
+  const auto all = host_clusters(b);
+  const auto owner = shard_owner(all, b, world);
+  for (int r = 0; r < world; ++r) pairs_per_rank[r] = 0;
+  for (size_t i = 0; i < all.size(); ++i) pairs_per_rank[owner[i]] += all[i].members;
+  return SO3_OK;
+}
+
+int so3_shard_cluster_owner(int b, int world, int32_t* owner_out) {
+  if (!valid_bandwidth(b) || world < 1 || !owner_out) return fail(SO3_ERR_INVALID, "bad arguments");
+  const auto all = host_clusters(b);
+  const auto owner = shard_owner(all, b, world);
+  for (size_t i = 0; i < all.size(); ++i) owner_out[i] = owner[i];
+  return SO3_OK;
+}
+
+int so3_shard_pair_list(int b, int world, int rank, int32_t* pairs_out) {
+  if (!valid_bandwidth(b) || world < 1 || rank < 0 || rank >= world || !pairs_out)
+    return fail(SO3_ERR_INVALID, "bad arguments");
+  const auto all = host_clusters(b);
+  const auto owner = shard_owner(all, b, world);
+  size_t k = 0;
+  for (size_t i = 0; i < all.size(); ++i) {
+    if (owner[i] != rank) continue;
+    for (const auto& pr : cluster_pairs(all[i].m, all[i].mp)) {
+      pairs_out[2 * k] = pr.first;
+      pairs_out[2 * k + 1] = pr.second;
+      ++k;
+    }
+  }
+  return SO3_OK;
+}
+
+int64_t so3_shard_slab_width(so3_plan_t p) { return p ? p->J : 0; }
+int64_t so3_shard_rank_pairs(so3_plan_t p) { return p ? p->pairs_rank : 0; }
 
 void so3_plan_destroy(so3_plan_t p) {
   if (!p) return;
@@ -504,6 +683,8 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_spec);
   cudaFree(p->d_rc);
   cudaFree(p->d_rc_off);
+  cudaFree(p->d_row_global);
+  cudaFree(p->d_row_local);
   cudaFree(p->d_grid_stage);
   cudaFree(p->d_coef_stage);
   delete p;
@@ -615,6 +796,35 @@ int so3_ifsoft_host(so3_plan_t p, const void* coeffs_host, void* samples_host, v
                            cudaMemcpyDeviceToHost, st));
   SO3_CUDA(cudaStreamSynchronize(st));
   return SO3_OK;
+}
+
+#define CHECK_SHARD(p) \
+  if (!(p)->sharded) return fail(SO3_ERR_INVALID, "not a sharded plan (so3_shard_plan_create)")
+
+int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(slab); CHECK_PTR(send);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = launch_fft(shard_pass_args(p, 0, slab, p->d_scratch), +1, 1, st, p->fft_wide);
+  if (rc) return rc;
+  return launch_fft(shard_pass_args(p, 1, p->d_scratch, send), +1, 1, st, p->fft_wide);
+}
+
+int so3_shard_dwt_analysis(so3_plan_t p, const void* recv, void* coeffs, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(recv); CHECK_PTR(coeffs);
+  return launch_dwt<true>(p, recv, coeffs, 0, p->nclusters, static_cast<cudaStream_t>(stream));
+}
+
+int so3_shard_dwt_synthesis(so3_plan_t p, const void* coeffs, void* send, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(coeffs); CHECK_PTR(send);
+  return launch_dwt<false>(p, send, const_cast<void*>(coeffs), 0, p->nclusters, static_cast<cudaStream_t>(stream));
+}
+
+int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(recv); CHECK_PTR(slab);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = launch_fft(shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st, p->fft_wide);
+  if (rc) return rc;
+  return launch_fft(shard_pass_args(p, 3, p->d_scratch, slab), -1, 1, st, p->fft_wide);
 }
 
 int so3_wigner_rows(so3_plan_t p, int m, int mp, double* out, void* stream) {

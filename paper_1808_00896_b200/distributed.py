@@ -1,0 +1,206 @@
+"""Sharded FSOFT / iFSOFT: one process per GPU, one all-to-all per direction.
+
+The reference parallelises inside one host with a fork pool (schedule.py:200-257) and joins
+its two stages with an in-memory transpose of the spectrum (soft.py:131-132, 142, 167).  Here
+G ranks split
+
+  * the torus FFT by beta slab  [rank*J, (rank+1)*J),  J = 2B / G  (the input/output samples
+    of a rank are grid[:, slab, :], laid out [i][jj][k]);
+  * the DWT by cost-balanced symmetry-cluster groups (LPT greedy over the launch schedule,
+    computed by the C library: so3_shard_*);
+
+and the transpose becomes one ``torch.distributed.all_to_all_single`` (NCCL over NVLink on a
+B200 box, gloo in the CPU tests).  Pack and unpack are fused into the FFT kernels through a
+pair -> row table, so the exchange moves the FFT output / DWT output buffers directly:
+
+  layout A  rows [rank g][pairs_g][J]      forward send, inverse recv
+  layout B  rows [rank h][pairs_rank][J]   forward recv, inverse send
+
+Results are bit-identical for every G (the same per-row FFTs and per-cluster reductions run
+whatever the split).  Coefficients stay sharded: a rank writes / reads only the slots of its
+clusters in a full-length array; ``gather_coefficients`` all-reduces them (each slot has one
+writer and zeros elsewhere, so the sum is exact).
+
+The stage kernels are supplied by a backend; ``NativeShardBackend`` calls the CUDA library.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Protocol
+
+import numpy as np
+
+from . import _native
+from .core import coeff_count, grid_size, validate_bandwidth
+
+
+class ShardMap:
+    """Host-side shard map of G ranks (no GPU needed): pairs per rank, slab width, splits."""
+
+    def __init__(self, bandwidth: int, world: int):
+        self.bandwidth = validate_bandwidth(bandwidth)
+        n = grid_size(self.bandwidth)
+        if world < 1 or n % world:
+            raise ValueError(f"2B={n} must be divisible by the number of ranks {world}")
+        self.world = world
+        self.n = n
+        self.J = n // world
+        counts = (ctypes.c_int64 * world)()
+        _native.check(_native.lib().so3_shard_pair_counts(self.bandwidth, world, counts), "shard_pair_counts")
+        self.pairs = [int(v) for v in counts]
+        assert sum(self.pairs) == (n - 1) ** 2
+
+    def pair_list(self, rank: int) -> np.ndarray:
+        out = np.empty((self.pairs[rank], 2), dtype=np.int32)
+        _native.check(_native.lib().so3_shard_pair_list(
+            self.bandwidth, self.world, rank, out.ctypes.data_as(_native._i32p)), "shard_pair_list")
+        return out
+
+    def cluster_owner(self) -> np.ndarray:
+        k = int(_native.lib().so3_cluster_count(self.bandwidth))
+        out = np.empty(k, dtype=np.int32)
+        _native.check(_native.lib().so3_shard_cluster_owner(
+            self.bandwidth, self.world, out.ctypes.data_as(_native._i32p)), "shard_cluster_owner")
+        return out
+
+    def layout_a_rows(self) -> int:
+        return sum(self.pairs)
+
+    def layout_b_rows(self, rank: int) -> int:
+        return self.world * self.pairs[rank]
+
+    # all_to_all_single split sizes, in complex128 elements
+    def forward_send_splits(self, rank: int) -> list[int]:
+        return [p * self.J for p in self.pairs]
+
+    def forward_recv_splits(self, rank: int) -> list[int]:
+        return [self.pairs[rank] * self.J] * self.world
+
+    def inverse_send_splits(self, rank: int) -> list[int]:
+        return self.forward_recv_splits(rank)
+
+    def inverse_recv_splits(self, rank: int) -> list[int]:
+        return self.forward_send_splits(rank)
+
+
+class ShardBackend(Protocol):
+    """The four stage kernels of one rank (buffer layouts above)."""
+
+    def fft_analysis(self, slab, send_a) -> None: ...
+    def dwt_analysis(self, recv_b, coeffs) -> None: ...
+    def dwt_synthesis(self, coeffs, send_b) -> None: ...
+    def fft_synthesis(self, recv_a, slab) -> None: ...
+    def empty(self, count: int): ...
+    def zeros(self, count: int): ...
+
+
+class NativeShardBackend:
+    """CUDA kernels of libso3fft_b200.so on the current device (torch complex128 tensors)."""
+
+    def __init__(self, bandwidth: int, world: int, rank: int, device=None):
+        import torch
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            torch.empty(1, device=self.device)
+            _native.check(_native.lib().so3_shard_plan_create(bandwidth, world, rank, ctypes.byref(handle)),
+                          "shard_plan_create")
+        self.handle = handle
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    @staticmethod
+    def _p(t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    def fft_analysis(self, slab, send_a):
+        _native.check(_native.lib().so3_shard_fft_analysis(self.handle, self._p(slab), self._p(send_a), self._stream()),
+                      "shard_fft_analysis")
+
+    def dwt_analysis(self, recv_b, coeffs):
+        _native.check(_native.lib().so3_shard_dwt_analysis(self.handle, self._p(recv_b), self._p(coeffs), self._stream()),
+                      "shard_dwt_analysis")
+
+    def dwt_synthesis(self, coeffs, send_b):
+        _native.check(_native.lib().so3_shard_dwt_synthesis(self.handle, self._p(coeffs), self._p(send_b), self._stream()),
+                      "shard_dwt_synthesis")
+
+    def fft_synthesis(self, recv_a, slab):
+        _native.check(_native.lib().so3_shard_fft_synthesis(self.handle, self._p(recv_a), self._p(slab), self._stream()),
+                      "shard_fft_synthesis")
+
+    def empty(self, count):
+        return self.torch.empty(count, dtype=self.torch.complex128, device=self.device)
+
+    def zeros(self, count):
+        return self.torch.zeros(count, dtype=self.torch.complex128, device=self.device)
+
+    def release(self):
+        if self.handle is not None:
+            _native.lib().so3_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def _as_real(t):
+    import torch
+    return torch.view_as_real(t).reshape(-1) if t.is_complex() else t
+
+
+class ShardedSO3:
+    """One rank of the sharded transform pair.  ``exchange`` defaults to all_to_all_single."""
+
+    def __init__(self, bandwidth: int, rank: int, world: int, backend: ShardBackend, group=None):
+        self.map = ShardMap(bandwidth, world)
+        self.bandwidth = self.map.bandwidth
+        self.rank, self.world = rank, world
+        self.backend = backend
+        self.group = group
+        self.coeff_count = coeff_count(self.bandwidth)
+        self.slab_count = self.map.n * self.map.J * self.map.n
+
+    def _all_to_all(self, recv, send, recv_splits, send_splits):
+        import torch.distributed as dist
+        if self.world == 1:
+            recv.copy_(send)
+            return
+        dist.all_to_all_single(_as_real(recv), _as_real(send),
+                               output_split_sizes=[2 * s for s in recv_splits],
+                               input_split_sizes=[2 * s for s in send_splits], group=self.group)
+
+    def fsoft(self, slab):
+        """This rank's beta slab [i][jj][k] -> coefficients (own slots; others zero)."""
+        m = self.map
+        send = self.backend.empty(m.layout_a_rows() * m.J)
+        self.backend.fft_analysis(slab, send)
+        recv = self.backend.empty(m.layout_b_rows(self.rank) * m.J)
+        self._all_to_all(recv, send, m.forward_recv_splits(self.rank), m.forward_send_splits(self.rank))
+        coeffs = self.backend.zeros(self.coeff_count)
+        self.backend.dwt_analysis(recv, coeffs)
+        return coeffs
+
+    def ifsoft(self, coeffs):
+        """Coefficients (this rank's slots are read) -> this rank's beta slab [i][jj][k]."""
+        m = self.map
+        send = self.backend.empty(m.layout_b_rows(self.rank) * m.J)
+        self.backend.dwt_synthesis(coeffs, send)
+        recv = self.backend.empty(m.layout_a_rows() * m.J)
+        self._all_to_all(recv, send, m.inverse_recv_splits(self.rank), m.inverse_send_splits(self.rank))
+        slab = self.backend.empty(self.slab_count)
+        self.backend.fft_synthesis(recv, slab)
+        return slab
+
+    def gather_coefficients(self, coeffs):
+        """Full coefficient array on every rank (exact: one writer per slot)."""
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(_as_real(coeffs), group=self.group)
+        return coeffs
