@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(128, MINB) dwt_synthesis_mma2_kernel(DwtArgs a
 
   if (t < 8) mem[t] = member_of(a, m, mp, t);
   __syncthreads();
-  const int nsteps = B - 1 - m;
+  const int nsteps = B - m;   // table entries (degrees)
   const int nq = (B - m + 3) >> 2;
   const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
 
@@ -91,8 +91,9 @@ __global__ void __launch_bounds__(128, MINB) dwt_synthesis_mma2_kernel(DwtArgs a
     const int s1 = ok1 ? coeff_slot32(lc, M1.pm, M1.pmp) : 0;
     const double v0 = __ldg(&coefd[2 * s0 + comp]);
     const double v1 = __ldg(&coefd[2 * s1 + comp]);
-    f0 = ok0 ? v0 : 0.0;
-    f1 = ok1 ? v1 : 0.0;
+    const double mu = (l < B) ? __ldg(&rct[3 * (l - m) + 2]) : 0.0;
+    f0 = ok0 ? v0 * mu : 0.0;
+    f1 = ok1 ? v1 * mu : 0.0;
   };
 
   const int jw0 = (crank * 4 + warp) * JW;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(128, MINB) dwt_synthesis_mma2_kernel(DwtArgs a
       for (int q = 0; q < JT; ++q) {
         D[ll * S + lane + 32 * q] = cur[q];
         const double tt = fma(k3.x, x[q], -k3.y);
-        const double nx = fma(tt, cur[q], -k3.z * prev[q]);
+        const double nx = fma(tt, cur[q], -prev[q]);
         prev[q] = cur[q];
         cur[q] = nx;
       }
@@ -202,7 +203,7 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
   if (t < 8) mem[t] = member_of(a, m, mp, t);
   if (t < R) { arrive[t] = 0; slot_free[t] = t; }
   __syncthreads();
-  const int nsteps = B - 1 - m;
+  const int nsteps = B - m;   // table entries (degrees)
   const int nb = (B - m + 7) >> 3;   // blocks of 8 degrees
   const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
 
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
       for (int q = 0; q < JT; ++q) {
         D[ll * S + lane + 32 * q] = cur[q];
         const double tt = fma(k3.x, x[q], -k3.y);
-        const double nx = fma(tt, cur[q], -k3.z * prev[q]);
+        const double nx = fma(tt, cur[q], -prev[q]);
         prev[q] = cur[q];
         cur[q] = nx;
       }
@@ -305,7 +306,7 @@ __global__ void __launch_bounds__(256, 1) dwt_analysis_mma2_kernel(DwtArgs a) {
             re += ps[w * 128 + o_re];
             im += ps[w * 128 + o_im];
           }
-          double sc = (2.0 * l + 1.0) / vscale;
+          double sc = (2.0 * l + 1.0) / vscale * __ldg(&rct[3 * (l - m) + 2]);   // v_l * mu_l
           if ((M.sl * l + M.par0) & 1) sc = -sc;
           coef[coeff_slot32(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
         }

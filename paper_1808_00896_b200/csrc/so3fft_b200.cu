@@ -139,6 +139,7 @@ struct so3_plan_s {
   int* d_row_global = nullptr;          // (m' bin)*n + (m bin) -> row of layout [rank g][pairs_g][J], -1 if none
   int* d_row_local = nullptr;           // same index -> row among this rank's pairs, -1 if not owned
   int dwt_variant = SO3_DWT_MMA;
+  int ana_cta = 1;    // analysis: single-CTA 32-degree-tile kernel (SO3_ANA_CTA=0: 2-CTA cluster kernel)
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
 };
@@ -317,8 +318,22 @@ int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned
 }
 
 template <int JW>
-int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+  using SM = so3::MmaSmem<JW>;
   const int warps = (n + JW - 1) / JW;
+  const size_t smem = ((size_t)warps * 16 * SM::S + 2 * (size_t)warps * 512) * sizeof(double);
+  auto k = so3::dwt_analysis_mma_cta_kernel<JW>;
+  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(ncl, batch), warps * 32, smem, st>>>(a);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+template <int JW>
+int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st,
+                   int ana_cta = 0) {
+  const int warps = (n + JW - 1) / JW;
+  if (analysis && ana_cta && warps <= 8) return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st);
   if (warps > (analysis ? 8 : 16)) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
   if (warps >= 4 && warps % 4 == 0) return launch_dwt_mma_wpc<JW, 4>(analysis, a, warps / 4, ncl, batch, st);
   if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2>(analysis, a, warps / 2, ncl, batch, st);
@@ -385,9 +400,9 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   }
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
-      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
-      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
-      default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
+      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
+      default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
     }
   }
   const int jt = dwt_jt(p->n);
@@ -502,7 +517,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   long long rc_entries = 0;
   for (size_t i = 0; i < cl.size(); ++i) {
     rc_off[i] = rc_entries;
-    rc_entries += std::max(1, b - 1 - cl[i].m);
+    rc_entries += b - cl[i].m;   // one (alpha, beta, mu) per degree
   }
   rc_entries = std::max(rc_entries, 1LL);
   std::vector<int2> bases(ncl, make_int2(0, 0));
@@ -548,7 +563,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   e = e ? e : cudaMemcpy(p->d_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_rc_off, rc_off.data(), ncl * sizeof(long long), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !cl.empty()) {
-    so3::rc_table_kernel<<<(unsigned)cl.size(), 128>>>(b, (int)cl.size(), p->d_bases, p->d_rc_off, p->d_rc);
+    so3::rc_table_kernel<<<(unsigned)((cl.size() + 127) / 128), 128>>>(b, (int)cl.size(), p->d_bases, p->d_rc_off, p->d_rc);
     e = cudaGetLastError();
   }
   e = e ? e : cudaDeviceSynchronize();
@@ -567,6 +582,7 @@ so3_plan_s* new_plan(int b, int batch) {
   cudaGetDevice(&p->device);
   if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
   if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
+  if (const char* e = getenv("SO3_ANA_CTA")) p->ana_cta = atoi(e);
   if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
   return p;
 }
