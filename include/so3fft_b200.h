@@ -164,6 +164,12 @@ int so3_shard_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* send_
 /* inverse: layout A -> slab (K4a with the unpack fused into the load, K4b) */
 int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_dev, void* stream);
 
+/* Direct O(B^6) transforms (fsoft_direct / ifsoft_direct, soft.py:212-256): the defining
+ * sums over closed-form Wigner functions (wigner.py:78-114), sharing nothing with the fast
+ * path; an independent cross-check for small B (1 <= B <= 64).  Synchronous on `stream`. */
+int so3_fsoft_direct(int bandwidth, const void* samples_dev, void* coeffs_dev, void* stream);
+int so3_ifsoft_direct(int bandwidth, const void* coeffs_dev, void* samples_dev, void* stream);
+
 /* Wigner rows d^l_{m,m'}(beta_j), l = max(|m|,|m'|)..B-1, j < 2B, for any pair
  * (wigner_d_rows, wigner.py:139-178 + derive_cluster_matrices, dwt.py:76-93):
  * out_dev[(l-L)*2B + j], generated by the same in-register recurrence as the DWT. */

@@ -26,6 +26,9 @@ from .core import (
     write_samples,
 )
 from .soft import (
+    DIRECT_BANDWIDTH_CAP,
+    fsoft_direct,
+    ifsoft_direct,
     OrderPair,
     QuadratureWeights,
     SampleAngles,

@@ -52,6 +52,8 @@ SIGNATURES = {
     "so3_plan_scratch": (_vp, [_vp]),
     "so3_plan_set_dwt_variant": (_c_int, [_vp, _c_int]),
     "so3_wigner_rows": (_c_int, [_vp, _c_int, _c_int, _vp, _vp]),
+    "so3_fsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),
+    "so3_ifsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),
     "so3_shard_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
     "so3_shard_slab_width": (_c_i64, [_vp]),
     "so3_shard_rank_pairs": (_c_i64, [_vp]),

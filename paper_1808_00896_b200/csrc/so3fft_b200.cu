@@ -22,6 +22,7 @@
 #include "dwt_mma.cuh"
 #include "dwt_mma2.cuh"
 #include "fft.cuh"
+#include "direct.cuh"
 
 namespace {
 
@@ -841,6 +842,59 @@ int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* st
   int rc = launch_fft(shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st, p->fft_wide);
   if (rc) return rc;
   return launch_fft(shard_pass_args(p, 3, p->d_scratch, slab), -1, 1, st, p->fft_wide);
+}
+
+// Direct O(B^6) transforms (soft.py:212-256): closed-form Wigner functions, no plan.
+static int direct_common(int b, double** d_betas, double** d_w, double** d_tab, cudaStream_t st) {
+  const int n = 2 * b;
+  const long long C = so3_coeff_count(b);
+  std::vector<double> betas(n), w(n);
+  for (int j = 0; j < n; ++j) betas[j] = (2.0 * j + 1.0) * 3.141592653589793 / (4.0 * b);   // quadrature.py:61
+  host_weights(b, w.data());
+  SO3_CUDA(cudaMalloc((void**)d_betas, n * sizeof(double)));
+  SO3_CUDA(cudaMalloc((void**)d_w, n * sizeof(double)));
+  SO3_CUDA(cudaMalloc((void**)d_tab, (size_t)C * n * sizeof(double)));
+  SO3_CUDA(cudaMemcpyAsync(*d_betas, betas.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  SO3_CUDA(cudaMemcpyAsync(*d_w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice, st));
+  const long long tot = C * n;
+  so3::direct_table_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(b, *d_betas, *d_tab);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int so3_ifsoft_direct(int b, const void* coeffs, void* samples, void* stream) {
+  if (!valid_bandwidth(b) || b > 64) return fail(SO3_ERR_INVALID, "direct transforms support 1 <= B <= 64");
+  CHECK_PTR(coeffs); CHECK_PTR(samples);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *be = nullptr, *w = nullptr, *tab = nullptr;
+  int rc = direct_common(b, &be, &w, &tab, st);
+  if (rc == SO3_OK) {
+    const long long tot = so3_grid_count(b);
+    so3::ifsoft_direct_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(
+        b, tab, static_cast<const double2*>(coeffs), static_cast<double2*>(samples));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(SO3_ERR_CUDA, std::string("ifsoft_direct: ") + cudaGetErrorString(e));
+  }
+  cudaFree(be); cudaFree(w); cudaFree(tab);
+  return rc;
+}
+
+int so3_fsoft_direct(int b, const void* samples, void* coeffs, void* stream) {
+  if (!valid_bandwidth(b) || b > 64) return fail(SO3_ERR_INVALID, "direct transforms support 1 <= B <= 64");
+  CHECK_PTR(coeffs); CHECK_PTR(samples);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *be = nullptr, *w = nullptr, *tab = nullptr;
+  int rc = direct_common(b, &be, &w, &tab, st);
+  if (rc == SO3_OK) {
+    so3::fsoft_direct_kernel<<<(unsigned)so3_coeff_count(b), 256, 0, st>>>(
+        b, tab, w, static_cast<const double2*>(samples), static_cast<double2*>(coeffs));
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(SO3_ERR_CUDA, std::string("fsoft_direct: ") + cudaGetErrorString(e));
+  }
+  cudaFree(be); cudaFree(w); cudaFree(tab);
+  return rc;
 }
 
 int so3_wigner_rows(so3_plan_t p, int m, int mp, double* out, void* stream) {

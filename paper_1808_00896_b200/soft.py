@@ -410,3 +410,37 @@ def wigner_rows(plan: TransformPlan, m: int, mp: int):
     out = torch.empty((b - lo, 2 * b), dtype=torch.float64, device=plan.device)
     _native.check(_native.lib().so3_wigner_rows(plan.handle, m, mp, _ptr(out), _stream(plan)), "wigner_rows")
     return out
+
+
+# ------------------------------------------------------------------ direct transforms (oracle route)
+
+DIRECT_BANDWIDTH_CAP = 12
+
+
+def _direct(data, bandwidth: int, max_bandwidth: int, out_count: int, fn: str):
+    """soft.py:196-201 cap semantics; runs the CUDA direct kernels on the current device."""
+    torch = _torch()
+    if bandwidth > max_bandwidth:
+        raise ValueError(f"direct transform capped at B={max_bandwidth} (got B={bandwidth}); "
+                         "raise max_bandwidth explicitly if you really want this")
+    host = not _is_torch(data)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    x = torch.from_numpy(np.ascontiguousarray(data, dtype=np.complex128)).to(dev) if host else data.contiguous()
+    out = torch.empty(out_count, dtype=torch.complex128, device=x.device)
+    with torch.cuda.device(x.device):
+        _native.check(getattr(_native.lib(), fn)(bandwidth, ctypes.c_void_p(x.data_ptr()),
+                                                 ctypes.c_void_p(out.data_ptr()),
+                                                 ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)), fn)
+    return out.cpu().numpy() if host else out
+
+
+def fsoft_direct(samples: So3SampleGrid, max_bandwidth: int = DIRECT_BANDWIDTH_CAP) -> So3Coefficients:
+    """Reference forward transform evaluated as the defining sum on the GPU (soft.py:212-233)."""
+    b = validate_bandwidth(samples.bandwidth)
+    return So3Coefficients(b, _direct(samples.data, b, max_bandwidth, coeff_count(b), "so3_fsoft_direct"))
+
+
+def ifsoft_direct(coeffs: So3Coefficients, max_bandwidth: int = DIRECT_BANDWIDTH_CAP) -> So3SampleGrid:
+    """Reference inverse transform evaluated as the defining sum on the GPU (soft.py:236-256)."""
+    b = validate_bandwidth(coeffs.bandwidth)
+    return So3SampleGrid(b, _direct(coeffs.data, b, max_bandwidth, grid_size(b) ** 3, "so3_ifsoft_direct"))

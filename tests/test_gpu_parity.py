@@ -334,3 +334,47 @@ def test_sofc_round_trip_through_transform(tmp_path):
     so3.write_samples(str(tmp_path / "g.sofg"), g)
     back = so3.fsoft_sequential(so3.read_samples(str(tmp_path / "g.sofg")), plan)
     assert np.abs(back.data - c.data).max() < 1e-12
+
+
+# ---------------------------------------------------------------- GPU direct route (row 8(f).4)
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4])
+def test_gpu_direct_matches_reference_direct(golden, b):
+    g = golden(f"soft_b{b}.npz")
+    inv = so3.ifsoft_direct(so3.So3Coefficients(b, g["coeffs"])).data
+    np.testing.assert_allclose(inv, g["direct_inverse"], atol=1e-13)
+    fwd = so3.fsoft_direct(so3.So3SampleGrid(b, g["raw_grid"])).data
+    np.testing.assert_allclose(fwd, g["direct_forward"], atol=1e-13)
+
+
+@pytest.mark.parametrize("b", [8, 12])
+def test_fast_path_matches_gpu_direct_route(b):
+    """Fast path vs the independent closed-form route, both on the GPU (acceptance criteria 1-2)."""
+    rng = np.random.default_rng(90 + b)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    plan = plan_for(b)
+    g_fast = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
+    g_dir = so3.ifsoft_direct(so3.So3Coefficients(b, c)).data
+    assert np.abs(g_fast - g_dir).max() < 1e-10
+    f_fast = so3.fsoft_sequential(so3.So3SampleGrid(b, g_dir), plan).data
+    f_dir = so3.fsoft_direct(so3.So3SampleGrid(b, g_dir)).data
+    assert np.abs(f_fast - f_dir).max() < 1e-10
+
+
+def test_gpu_direct_cap():
+    with pytest.raises(ValueError):
+        so3.fsoft_direct(so3.So3SampleGrid.zeros(13))
+    out = so3.ifsoft_direct(so3.So3Coefficients.zeros(2), max_bandwidth=2)
+    assert out.bandwidth == 2
+
+
+def test_report_harness_on_gpu(tmp_path):
+    """so3fft-bench protocol on the GPU path, with the direct-route oracle (bench.py:146-209)."""
+    from paper_1808_00896_b200 import report as R
+    cfg = R.BenchConfig([4, 8], [1, 2], runs=2, seed=3, oracle=True)
+    recs = R.run_benchmark(cfg, str(tmp_path / "g.sofg"), str(tmp_path / "c.sofc"))
+    assert len(recs) == 2 * 2 * 2 * 2
+    assert all(r.max_abs_error < 1e-12 for r in recs)
+    assert (tmp_path / "g.sofg").exists() and (tmp_path / "c.sofc").exists()
+    assert R.main(["--bandwidths", "4", "--threads", "1", "--runs", "1", "--oracle",
+                   "--output", str(tmp_path / "r.csv")]) == 0
