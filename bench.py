@@ -229,16 +229,19 @@ def run_reference_arm(args, rank: int, world: int) -> None:
 
 # --------------------------------------------------------------------------- GPU arm
 
-def metric_name(b: int) -> str:
-    return f"FSOFT+iFSOFT transforms/sec (B={b}, fp64)"
+def metric_name(b: int, batch: int = 1) -> str:
+    return f"FSOFT+iFSOFT transforms/sec (B={b}{f', batch {batch}' if batch > 1 else ''}, fp64)"
 
 
-def workload_config(b: int, world: int) -> dict:
-    return {"workload": f"BASELINE configs: B={b} single function, complex128, coefficients N(0,1) seed={b}; "
-                        "iFSOFT then FSOFT", "bandwidth": b, "functions_per_step": 1,
-            "grid": f"{2 * b}^3 complex128 ({16 * (2 * b) ** 3 / 1e9:.2f} GB)",
-            "coefficients": coeff_count(b),
-            "l2": "inputs larger than L2 (126 MB)" if 16 * (2 * b) ** 3 > 126e6 else "L2 flushed between steps",
+def workload_config(b: int, world: int, batch: int = 1) -> dict:
+    if batch == 1:
+        what = f"B={b} single function, complex128, coefficients N(0,1) seed={b}"
+    else:
+        what = f"B={b}, batch of {batch} functions, coefficients N(0,1) seeds 32000+f scaled by 1/(1+l)"
+    return {"workload": f"BASELINE configs: {what}; iFSOFT then FSOFT", "bandwidth": b, "functions_per_step": batch,
+            "grid": f"{batch} x {2 * b}^3 complex128 ({batch * 16 * (2 * b) ** 3 / 1e9:.2f} GB)",
+            "coefficients": coeff_count(b) * batch,
+            "l2": "inputs larger than L2 (126 MB)" if batch * 16 * (2 * b) ** 3 > 126e6 else "L2 flushed between steps",
             "parallelism": f"replicas x{world}" if world > 1 else "single GPU"}
 
 
@@ -256,17 +259,22 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     b = args.bandwidth
     n = 2 * b
     C = coeff_count(b)
-    plan = so3.make_plan(b, device=dev)
+    F = args.batch
+    plan = so3.make_plan(b, device=dev, batch=F)
     plan.set_dwt_variant(args.dwt_variant)
     stream = torch.cuda.current_stream(dev)
 
-    host_c = seeded_coefficients(b, b)
+    if F == 1:
+        host_c = seeded_coefficients(b, b)
+    else:   # BASELINE configs[1]: seeds 32000 + f, scaled by 1/(1+l)
+        scale = 1.0 / (1.0 + np.repeat(np.arange(b), [(2 * l + 1) ** 2 for l in range(b)]))
+        host_c = np.concatenate([seeded_coefficients(b, 32000 + f) * scale for f in range(F)])
     coeffs = torch.from_numpy(host_c).to(dev)
-    grid = torch.empty(n ** 3, dtype=torch.complex128, device=dev)
-    spec = torch.empty(n ** 3, dtype=torch.complex128, device=dev)
-    out = torch.empty(C, dtype=torch.complex128, device=dev)
+    grid = torch.empty(F * n ** 3, dtype=torch.complex128, device=dev)
+    spec = torch.empty(F * n ** 3, dtype=torch.complex128, device=dev)
+    out = torch.empty(F * C, dtype=torch.complex128, device=dev)
     flush = None
-    if 16 * n ** 3 <= 126e6 * 2:
+    if 16 * F * n ** 3 <= 126e6 * 2:
         flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MB > L2
 
     n_ev = 5
@@ -318,7 +326,7 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = world * 2.0 * 1000.0 / ms_step
+    value = world * F * 2.0 * 1000.0 / ms_step
 
     # parity of the measured output: round trip recovers the seeded coefficients
     got = out.cpu().numpy()
@@ -330,13 +338,17 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     # end to end through the public API with pinned host buffers (the reference's numpy contract)
     e2e = None
     if not args.no_e2e:
-        h_c = torch.empty(C, dtype=torch.complex128, pin_memory=True).numpy()
+        h_c = torch.empty(F * C, dtype=torch.complex128, pin_memory=True).numpy()
         h_c[:] = host_c
-        h_g = torch.empty(n ** 3, dtype=torch.complex128, pin_memory=True).numpy()
-        h_o = torch.empty(C, dtype=torch.complex128, pin_memory=True).numpy()
+        h_g = torch.empty(F * n ** 3, dtype=torch.complex128, pin_memory=True).numpy()
+        h_o = torch.empty(F * C, dtype=torch.complex128, pin_memory=True).numpy()
         def e2e_step():
-            g = so3.ifsoft_sequential(so3.So3Coefficients(b, h_c), plan, out=h_g)
-            so3.fsoft_sequential(so3.So3SampleGrid(b, g.data), plan, out=h_o)
+            if F == 1:
+                g = so3.ifsoft_sequential(so3.So3Coefficients(b, h_c), plan, out=h_g)
+                so3.fsoft_sequential(so3.So3SampleGrid(b, g.data), plan, out=h_o)
+            else:
+                so3.ifsoft_batch(h_c, plan, out=h_g)
+                so3.fsoft_batch(h_g, plan, out=h_o)
         for _ in range(max(1, min(args.warmup, 2))):
             e2e_step()
         if dist is not None:
@@ -356,8 +368,8 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e_err = float(np.abs(h_o - host_c).max())
-        e2e = {"value": world * 2000.0 / e_ms, "unit": "transforms/s", "ms_per_step": e_ms,
-               "h2d_bytes_per_step": 16 * (C + n ** 3), "d2h_bytes_per_step": 16 * (n ** 3 + C),
+        e2e = {"value": world * F * 2000.0 / e_ms, "unit": "transforms/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": 16 * F * (C + n ** 3), "d2h_bytes_per_step": 16 * F * (n ** 3 + C),
                "steps": ksteps, "roundtrip_max_abs": e2e_err,
                "api": "ifsoft_sequential(So3Coefficients numpy, pinned) -> fsoft_sequential(So3SampleGrid numpy)"}
 
@@ -366,8 +378,8 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     peaks = measured_peaks()
     p64 = peaks["fp64_tflops"] * 1e12
     bw = peaks["hbm_gbs"] * 1e9
-    fl = dwt_flops(b)
-    by = fft_bytes(b)
+    fl = dwt_flops(b) * F
+    by = fft_bytes(b) * F
     dom = max(("dwt_analysis", "dwt_synthesis"), key=lambda k: stage_ms[k])
     achieved = fl / (stage_ms[dom] * 1e-3) / 1e12
     traffic = None
@@ -379,7 +391,7 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
             "bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
             "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
             "peak_source": peaks["fp64_source"],
-            "algorithmic": f"8*B*C(B) = {fl:.4g} flop per launch (one transform direction)"}
+            "algorithmic": f"8*B*C(B) x {F} functions = {fl:.4g} flop per launch (one transform direction)"}
     stages = {}
     for nm in stage_names:
         ms = stage_ms[nm]
@@ -391,19 +403,19 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     cpu = None
     if world == 1 and not args.no_cpu:
         from oracle import so3_oracle as O
-        r = cpu_sample_rate(b, 4242, O.default_workers(), args.cpu_slices, args.cpu_clusters)
+        r = cpu_sample_rate(b, 4242, O.default_workers(), args.cpu_slices, args.cpu_clusters)   # per function
         cpu = {"value": r["transforms_per_s"], "unit": "transforms/s", "cores": O.default_workers(),
                "kind": "port", "sample": r["sample"],
                "est_seconds": {"inverse": r["inverse"], "forward": r["forward"]}}
     line = {
-        "metric": metric_name(b), "value": value, "unit": "transforms/s", "n_gpus": world,
+        "metric": metric_name(b, F), "value": value, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(b, world),
-        "fsoft_per_s": world * 1000.0 / (stage_ms["fft_analysis"] + stage_ms["dwt_analysis"]),
-        "ifsoft_per_s": world * 1000.0 / (stage_ms["dwt_synthesis"] + stage_ms["fft_synthesis"]),
+        "config": workload_config(b, world, F),
+        "fsoft_per_s": world * F * 1000.0 / (stage_ms["fft_analysis"] + stage_ms["dwt_analysis"]),
+        "ifsoft_per_s": world * F * 1000.0 / (stage_ms["dwt_synthesis"] + stage_ms["fft_synthesis"]),
         "stages": stages, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-        "gpu_launches": 6 * args.steps,
+        "gpu_launches": (6 + (1 if flush is not None else 0)) * args.steps,
         "clocks": clk,
         "parity": {"roundtrip_max_abs": rt_abs, "roundtrip_max_rel_per_slot": rt_rel,
                    "roundtrip_max_rel_of_max": rt_rel_max},
@@ -520,8 +532,9 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--bandwidth", "-B", type=int, default=DEFAULT_B)
+    ap.add_argument("--batch", type=int, default=1, help="functions per step (BASELINE configs[1]: B=32, 64)")
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--dwt-variant", choices=("mma", "mma2", "simt"), default="mma")
+    ap.add_argument("--dwt-variant", choices=("mma", "simt"), default="mma")
     ap.add_argument("--mode", choices=("auto", "single", "sharded", "replicas"), default="auto",
                     help="auto: single GPU at N=1, sharded (one transform over N GPUs) at N>1")
     ap.add_argument("--no-e2e", action="store_true")

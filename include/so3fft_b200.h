@@ -126,13 +126,15 @@ int so3_dwt_analysis(so3_plan_t plan, const void* spectrum_dev, void* coeffs_dev
 int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_dev,
                       int64_t cluster_begin, int64_t cluster_end, void* stream);
 
-/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4), SO3_DWT_MMA2 (DMMA,
- * barrier-free ring reduction) or SO3_DWT_SIMT (DFMA + warp butterfly).  Same results
- * to rounding. */
+/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4) or SO3_DWT_SIMT (DFMA +
+ * warp butterfly).  Same results to rounding. */
 #define SO3_DWT_MMA 0
 #define SO3_DWT_SIMT 1
-#define SO3_DWT_MMA2 2
 int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
+/* Tuning knobs (same results, different kernel shapes): "dwt_variant", "ana_cta" (analysis
+ * kernel: 1 single-CTA 32-degree tiles, 0 two-CTA cluster), "syn_jw" (synthesis beta indices
+ * per warp, 0 = default), "fft_xb" (FFT rows per CTA, 0 = default). */
+int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */
 void* so3_plan_scratch(so3_plan_t plan);

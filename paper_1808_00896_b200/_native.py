@@ -51,6 +51,7 @@ SIGNATURES = {
     "so3_dwt_synthesis": (_c_int, [_vp, _vp, _vp, _c_i64, _c_i64, _vp]),
     "so3_plan_scratch": (_vp, [_vp]),
     "so3_plan_set_dwt_variant": (_c_int, [_vp, _c_int]),
+    "so3_plan_set_knob": (_c_int, [_vp, ctypes.c_char_p, _c_int]),
     "so3_wigner_rows": (_c_int, [_vp, _c_int, _c_int, _vp, _vp]),
     "so3_fsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),
     "so3_ifsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),

@@ -20,7 +20,6 @@
 #include "common.cuh"
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
-#include "dwt_mma2.cuh"
 #include "fft.cuh"
 #include "direct.cuh"
 
@@ -288,7 +287,7 @@ int dwt_jw(int n) {
   return 32;
 }
 
-template <int JW, int WPC>
+template <int JW, int WPC, int FG = 1>
 int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
   if (analysis) {
@@ -310,22 +309,22 @@ int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned
     SO3_CUDA(cudaLaunchKernelEx(&cfg, k, a));
   } else {
     const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
-    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2)>;
+    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG>;
     SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<dim3(ncl * split, batch), WPC * 32, smem, st>>>(a, split);
+    k<<<dim3(ncl * split, batch / FG), WPC * 32, smem, st>>>(a, split);
   }
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
 
-template <int JW>
+template <int JW, int FG = 1>
 int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
   const int warps = (n + JW - 1) / JW;
-  const size_t smem = ((size_t)warps * 16 * SM::S + 2 * (size_t)warps * 512) * sizeof(double);
-  auto k = so3::dwt_analysis_mma_cta_kernel<JW>;
+  const size_t smem = ((size_t)warps * 16 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
+  auto k = so3::dwt_analysis_mma_cta_kernel<JW, FG>;
   SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<dim3(ncl, batch), warps * 32, smem, st>>>(a);
+  k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
@@ -334,32 +333,15 @@ template <int JW>
 int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st,
                    int ana_cta = 0) {
   const int warps = (n + JW - 1) / JW;
+  if (JW == 32 && batch % 4 == 0 && !analysis) {   // batched small B: 4 functions share each recurrence
+    if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2, 4>(analysis, a, warps / 2, ncl, batch, st);
+    return launch_dwt_mma_wpc<JW, 1, 4>(analysis, a, warps, ncl, batch, st);
+  }
   if (analysis && ana_cta && warps <= 8) return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st);
   if (warps > (analysis ? 8 : 16)) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
   if (warps >= 4 && warps % 4 == 0) return launch_dwt_mma_wpc<JW, 4>(analysis, a, warps / 4, ncl, batch, st);
   if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2>(analysis, a, warps / 2, ncl, batch, st);
   return launch_dwt_mma_wpc<JW, 1>(analysis, a, warps, ncl, batch, st);
-}
-
-template <int JW>
-int launch_dwt_mma2(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
-  using K = so3::Mma2<JW>;
-  const int warps = (n + JW - 1) / JW;
-  if (analysis) {
-    if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA2 analysis kernel");
-    const size_t smem = ((size_t)warps * K::ana_warp_doubles + (size_t)K::R * warps * 128) * sizeof(double);
-    auto k = so3::dwt_analysis_mma2_kernel<JW>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<dim3(ncl, batch), warps * 32, smem, st>>>(a);
-  } else {
-    const int split = (warps + 3) / 4;
-    const size_t smem = 4 * K::syn_warp_doubles * sizeof(double);
-    auto k = so3::dwt_synthesis_mma2_kernel<JW, (JW >= 128 ? 2 : 4)>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<dim3(ncl * split, batch), 128, smem, st>>>(a, split);
-  }
-  SO3_CUDA(cudaGetLastError());
-  return SO3_OK;
 }
 
 template <bool ANALYSIS>
@@ -386,18 +368,10 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.J = p->sharded ? p->J : p->n;
   a.slab_stride = p->sharded ? (long long)p->pairs_rank * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
-  if (p->dwt_variant == SO3_DWT_MMA2 && p->n <= 1024 && p->B <= 812) {
-    const int jw = ANALYSIS ? (p->n >= 1024 ? 128 : p->n >= 512 ? 64 : 32)
-                            : (p->n >= 512 ? 128 : p->n >= 256 ? 64 : 32);
-    switch (jw) {
-      case 128: return launch_dwt_mma2<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
-      case 64: return launch_dwt_mma2<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
-      default: return launch_dwt_mma2<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
-    }
-  }
-  if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && p->syn_jw && (p->n + p->syn_jw - 1) / p->syn_jw <= 16) {
-    if (p->syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
-    if (p->syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
+  const int syn_jw = p->syn_jw ? p->syn_jw : (p->n == 512 ? 64 : 0);
+  if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && syn_jw && (p->n + syn_jw - 1) / syn_jw <= 16) {
+    if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
+    if (syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
   }
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
@@ -713,10 +687,19 @@ int so3_plan_device(so3_plan_t p) { return p ? p->device : -1; }
 int64_t so3_plan_device_bytes(so3_plan_t p) { return p ? p->bytes : 0; }
 void* so3_plan_scratch(so3_plan_t p) { return p ? p->d_spec : nullptr; }
 
+int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
+  if (!p || !name) return fail(SO3_ERR_INVALID, "null plan or knob name");
+  const std::string k(name);
+  if (k == "dwt_variant") return so3_plan_set_dwt_variant(p, value);
+  if (k == "ana_cta") { p->ana_cta = value; return SO3_OK; }
+  if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
+  if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
+  return fail(SO3_ERR_INVALID, "unknown knob " + k);
+}
+
 int so3_plan_set_dwt_variant(so3_plan_t p, int variant) {
   if (!p) return fail(SO3_ERR_INVALID, "null plan");
-  if (variant != SO3_DWT_MMA && variant != SO3_DWT_SIMT && variant != SO3_DWT_MMA2)
-    return fail(SO3_ERR_INVALID, "unknown DWT variant");
+  if (variant != SO3_DWT_MMA && variant != SO3_DWT_SIMT) return fail(SO3_ERR_INVALID, "unknown DWT variant");
   p->dwt_variant = variant;
   return SO3_OK;
 }

@@ -213,11 +213,15 @@ class TransformPlan:
         return self._handle
 
     def set_dwt_variant(self, variant: str) -> None:
-        """DWT kernel family: "mma" (default: FP64 DMMA), "mma2" (DMMA, pipelined) or "simt" (DFMA)."""
-        code = {"mma": 0, "simt": 1, "mma2": 2}.get(variant)
+        """DWT kernel family: "mma" (default: FP64 DMMA) or "simt" (DFMA + warp butterfly)."""
+        code = {"mma": 0, "simt": 1}.get(variant)
         if code is None:
             raise ValueError(f"unknown DWT variant {variant!r}")
         _native.check(_native.lib().so3_plan_set_dwt_variant(self.handle, code), "set_dwt_variant")
+
+    def set_knob(self, name: str, value: int) -> None:
+        """Tuning knob of the native plan (see include/so3fft_b200.h so3_plan_set_knob)."""
+        _native.check(_native.lib().so3_plan_set_knob(self.handle, name.encode(), int(value)), "set_knob")
 
     @property
     def device_bytes(self) -> int:

@@ -31,7 +31,7 @@ def per_slot(got, ref):
     return O.error_metrics(ref, np.asarray(got))[1]
 
 
-@pytest.fixture(scope="module", params=["mma2", "mma", "simt"])
+@pytest.fixture(scope="module", params=["mma", "simt"])
 def variant(request):
     return request.param
 

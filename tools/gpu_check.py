@@ -13,7 +13,7 @@ for b in [int(x) for x in (sys.argv[1:] or [1, 2, 3, 4, 5, 6, 8, 16, 32, 64])]:
     C = O.n_coeffs(b)
     c = rng.standard_normal(C) + 1j * rng.standard_normal(C)
     plan = so3.make_plan(b)
-    plan.set_dwt_variant(os.environ.get('SO3_DWT', 'mma2'))
+    plan.set_dwt_variant(os.environ.get('SO3_DWT', 'mma'))
     t0 = time.time()
     g = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
     f = so3.fsoft_sequential(so3.So3SampleGrid(b, g), plan).data
