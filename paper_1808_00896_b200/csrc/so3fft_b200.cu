@@ -321,7 +321,7 @@ template <int JW, int FG = 1>
 int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
   const int warps = (n + JW - 1) / JW;
-  const size_t smem = ((size_t)warps * 16 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
+  const size_t smem = ((size_t)warps * 8 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, FG>;
   SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a);

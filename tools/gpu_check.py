@@ -14,6 +14,8 @@ for b in [int(x) for x in (sys.argv[1:] or [1, 2, 3, 4, 5, 6, 8, 16, 32, 64])]:
     c = rng.standard_normal(C) + 1j * rng.standard_normal(C)
     plan = so3.make_plan(b)
     plan.set_dwt_variant(os.environ.get('SO3_DWT', 'mma'))
+    for kv in filter(None, os.environ.get('SO3_KNOBS', '').split(',')):
+        k, v = kv.split('='); plan.set_knob(k, int(v))
     t0 = time.time()
     g = so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan).data
     f = so3.fsoft_sequential(so3.So3SampleGrid(b, g), plan).data
