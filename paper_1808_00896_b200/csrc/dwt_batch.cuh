@@ -1,0 +1,276 @@
+// Batched DWT for small bandwidths (BASELINE configs[1]: B = 32, 64 functions; reference
+// dwt.py:109-125 applied per function, soft.py:134-167).
+//
+// With many functions sharing one plan, the DWT of a symmetry cluster is a dense contraction
+// over the SAME Wigner matrix D[l][j] (l = m..B-1, j < 2B):
+//
+//   analysis   C[l][(f, member, re/im)] = sum_j  D[l][j] * S_f(member, j or mirror)
+//   synthesis  G[j][(f, member, re/im)] = sum_l  D[l][j] * sign * mu_l * F_f(l, member)
+//
+// One CTA takes one cluster and FC functions (one warp per function).  Per tile of 32 degrees
+// the threads run the rescaled recurrence once (one beta index per thread) into a shared
+// Wigner tile; every warp then contracts it with its function on the FP64 tensor path
+// (DMMA m8n8k4), so the seeds, the recurrence and the member table are paid once per FC
+// functions and no cross-warp reduction is needed (each warp owns the full j range).  The
+// spectrum of the FC functions (analysis) or their signed coefficients (synthesis) is staged
+// in shared memory with coalesced loads.  Shared rows are padded to a stride = 4 (mod 16)
+// doubles so both fragment reads are bank-conflict free.
+//
+// Same arithmetic as dwt_mma.cuh: the synthesis sums degree quads from l = m upward exactly
+// like the single-function kernel (results are bit-identical to it); the analysis sums j in
+// one pass per warp (the single-function kernel splits j over warps), so it agrees to rounding.
+#pragma once
+#include "common.cuh"
+#include "dwt.cuh"
+#include "dwt_mma.cuh"
+
+namespace so3 {
+
+__host__ __device__ inline int batch_np(int n) { return (n + 7) & ~7; }
+__host__ __device__ inline int batch_sd(int n) {   // >= np, = 4 (mod 16) when np = 0 (mod 16)
+  const int np = batch_np(n);
+  return np + ((4 - np) & 15);
+}
+
+// Wigner tile rows l0 .. l0+31 of the cluster for this thread's j (rows past B-1 are zero);
+// recurrence table entries come through L1 (every thread of the CTA reads the same ones).
+__device__ __forceinline__ void batch_wigner_tile_ldg(double* D, int sd, int t, int nl, const double* rct, int l0m,
+                                                      double x, double& cur, double& prev) {
+#pragma unroll 4
+  for (int ll = 0; ll < 32; ++ll) {
+    if (ll < nl) {
+      D[ll * sd + t] = cur;
+      const double tt = fma(__ldg(&rct[3 * (l0m + ll)]), x, -__ldg(&rct[3 * (l0m + ll) + 1]));
+      const double nx = fma(tt, cur, -prev);
+      prev = cur;
+      cur = nx;
+    } else {
+      D[ll * sd + t] = 0.0;
+    }
+  }
+}
+
+template <int FC>
+__host__ __device__ inline size_t batch_analysis_smem(int n) {
+  return (size_t)(32 + FC * 16) * batch_sd(n) * sizeof(double);
+}
+template <int FC>
+__host__ __device__ inline size_t batch_synthesis_smem(int n) {
+  return ((size_t)32 * batch_sd(n) + (size_t)32 * (FC * 16 + 4)) * sizeof(double);
+}
+
+// ---------------------------------------------------------------------------------- analysis
+// Warp w stages and contracts function f0 + w only: its spectrum rows never need a CTA
+// barrier, only the shared Wigner tile does.
+template <int FC, int CHK>
+__global__ void __launch_bounds__(FC * 32, 2) dwt_analysis_batch_kernel(DwtArgs a, int batch) {
+  extern __shared__ double dsm[];
+  __shared__ Member mem[8];
+  const int c = a.cluster0 + blockIdx.x;
+  const int f0 = blockIdx.y * FC;
+  const int2 base = __ldg(&a.bases[c]);
+  const int m = base.x, mp = base.y;
+  const int B = a.B, n = a.n, np = batch_np(n), sd = batch_sd(n);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int fl = warp;
+  const bool fvalid = f0 + fl < batch;
+  double* D = dsm;                                   // [32][sd]
+  double* Sf = dsm + 32 * sd + fl * 16 * sd;         // this warp's [16][sd]: column 2k + (re, im)
+  if (t < 8) mem[t] = member_of(a, m, mp, t);
+  __syncthreads();
+
+  // spectrum rows of the 8 members (mirrored for reflecting members), 4 members x CHK
+  // chunks of 32 beta in flight per pass; zero past n and for missing members / functions
+  const double2* spec = a.spec + (long long)(f0 + fl) * a.spec_fstride;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    double2 v[4][CHK];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const Member M = mem[4 * half + kk];
+#pragma unroll
+      for (int ch = 0; ch < CHK; ++ch) {
+        const int j = lane + 32 * ch;
+        v[kk][ch] = (fvalid && M.valid && j < n) ? spec[spec_index(a, M.row, j)] : make_double2(0.0, 0.0);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+      const int k = 4 * half + kk;
+      const bool refl = mem[k].reflect;
+#pragma unroll
+      for (int ch = 0; ch < CHK; ++ch) {
+        const int j = lane + 32 * ch;
+        if (j < np) {
+          const int jj = (j < n && refl) ? n - 1 - j : j;
+          Sf[(2 * k) * sd + jj] = v[kk][ch].x;
+          Sf[(2 * k + 1) * sd + jj] = v[kk][ch].y;
+        }
+      }
+    }
+  }
+
+  const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
+  double x = 0.0, cur = 0.0, prev = 0.0;
+  if (t < n) {
+    x = __ldg(&a.cosb[t]);
+    cur = seed_value(m, mp, __ldg(&a.lnorm[c]), a.logcs[t]);
+  }
+  const bool two_tiles = mem[4].valid;
+  const double vscale = 8.0 * 3.141592653589793 * (double)B;
+  double2* coef = a.coef + (long long)(f0 + fl) * a.coef_fstride;
+
+  for (int l0 = m; l0 < B; l0 += 32) {
+    const int nl = min(32, B - l0);
+    if (l0 > m) __syncthreads();   // every warp is done reading the previous tile
+    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, cur, prev);
+    __syncthreads();               // tile (and, first time, every warp's own staging) visible
+    if (!fvalid) continue;
+    const int mtn = (nl + 7) >> 3;
+    double acc[4][2][2];
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+    const double* Dg = D + g * sd + tq;
+    const double* S0 = Sf + g * sd + tq;
+    const double* S1 = Sf + (8 + g) * sd + tq;
+    if (two_tiles) {
+#pragma unroll 4
+      for (int jc = 0; jc < np; jc += 4) {
+        const double b0 = S0[jc], b1 = S1[jc];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+          if (mt < mtn) {
+            const double av = Dg[8 * mt * sd + jc];
+            dmma884(acc[mt][0][0], acc[mt][0][1], av, b0);
+            dmma884(acc[mt][1][0], acc[mt][1][1], av, b1);
+          }
+      }
+    } else {
+#pragma unroll 4
+      for (int jc = 0; jc < np; jc += 4) {
+        const double b0 = S0[jc];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+          if (mt < mtn) dmma884(acc[mt][0][0], acc[mt][0][1], Dg[8 * mt * sd + jc], b0);
+      }
+    }
+    // C[l = l0 + 8 mt + g][col = 8 nt + 2 tq + e]: member 4 nt + tq, (re, im)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int l = l0 + 8 * mt + g;
+      if (mt >= mtn || l >= B) continue;
+      const double vmu = (2.0 * l + 1.0) / vscale * __ldg(&rct[3 * (l - m) + 2]);   // v_l * mu_l
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const Member M = mem[4 * nt + tq];
+        if (!M.valid) continue;
+        const double sc = ((M.sl * l + M.par0) & 1) ? -vmu : vmu;
+        coef[coeff_slot(l, M.pm, M.pmp)] = make_double2(acc[mt][nt][0] * sc, acc[mt][nt][1] * sc);
+      }
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------- synthesis
+// Warp w stages the signed coefficients of function f0 + w (8 per lane per 32-degree tile,
+// fetched one tile ahead) and owns its output; only the Wigner tile is shared.
+template <int FC, int MTMAX>
+__global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs a, int batch) {
+  constexpr int SF = FC * 16 + 4;
+  extern __shared__ double dsm[];
+  __shared__ Member mem[8];
+  const int c = a.cluster0 + blockIdx.x;
+  const int f0 = blockIdx.y * FC;
+  const int2 base = __ldg(&a.bases[c]);
+  const int m = base.x, mp = base.y;
+  const int B = a.B, n = a.n, np = batch_np(n), sd = batch_sd(n);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int fl = warp;
+  const bool fvalid = f0 + fl < batch;
+  double* D = dsm;                         // [32][sd]
+  double* Ff = dsm + 32 * sd + fl * 16;    // [32][SF] rows, this warp's 16 columns
+  if (t < 8) mem[t] = member_of(a, m, mp, t);
+  __syncthreads();
+
+  const double* rct = a.rc + 3 * __ldg(&a.rc_off[c]);
+  const double2* coef = a.coef + (long long)(f0 + fl) * a.coef_fstride;
+  const int k = lane & 7;                  // this lane's member; degrees ll = (lane >> 3) + 4 i
+  const Member Mk = mem[k];
+  double2 z[8];
+  auto fetch = [&](int l0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int l = l0 + (lane >> 3) + 4 * i;
+      z[i] = (fvalid && Mk.valid && l < B) ? coef[coeff_slot(l, Mk.pm, Mk.pmp)] : make_double2(0.0, 0.0);
+    }
+  };
+  fetch(m);
+
+  double x = 0.0, cur = 0.0, prev = 0.0;
+  if (t < n) {
+    x = __ldg(&a.cosb[t]);
+    cur = seed_value(m, mp, __ldg(&a.lnorm[c]), a.logcs[t]);
+  }
+  const bool two_tiles = mem[4].valid;
+  const int mtn = np >> 3;
+  double acc[MTMAX][2][2];
+#pragma unroll
+  for (int mt = 0; mt < MTMAX; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  for (int l0 = m; l0 < B; l0 += 32) {
+    const int nl = min(32, B - l0);
+    if (l0 > m) __syncthreads();   // every warp is done reading the previous Wigner tile
+    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, cur, prev);
+    // this warp's signed, mu-scaled coefficients of the tile (its own previous reads are
+    // complete: same warp, program order)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ll = (lane >> 3) + 4 * i, l = l0 + ll;
+      double sg = 0.0;
+      if (l < B) {
+        const double mu = __ldg(&rct[3 * (l - m) + 2]);
+        sg = ((Mk.sl * l + Mk.par0) & 1) ? -mu : mu;
+      }
+      Ff[ll * SF + 2 * k] = z[i].x * sg;
+      Ff[ll * SF + 2 * k + 1] = z[i].y * sg;
+    }
+    if (l0 + 32 < B) fetch(l0 + 32);
+    __syncthreads();
+    if (!fvalid) continue;
+    const double* Fb = Ff + tq * SF + g;
+    const double* Da = D + tq * sd + g;
+    for (int s = 0; s < ((nl + 3) >> 2); ++s) {
+      const double b0 = Fb[4 * s * SF];
+      const double b1 = two_tiles ? Fb[4 * s * SF + 8] : 0.0;
+#pragma unroll
+      for (int mt = 0; mt < MTMAX; ++mt) {
+        if (mt < mtn) {
+          const double av = Da[4 * s * sd + 8 * mt];
+          dmma884(acc[mt][0][0], acc[mt][0][1], av, b0);
+          if (two_tiles) dmma884(acc[mt][1][0], acc[mt][1][1], av, b1);
+        }
+      }
+    }
+  }
+  if (!fvalid) return;
+  // G[j = 8 mt + g][col = 8 nt + 2 tq + e]: member 4 nt + tq at j (or its mirror)
+  double2* spec = const_cast<double2*>(a.spec) + (long long)(f0 + fl) * a.spec_fstride;
+#pragma unroll
+  for (int mt = 0; mt < MTMAX; ++mt) {
+    const int j = 8 * mt + g;
+    if (mt >= mtn || j >= n) continue;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const Member M = mem[4 * nt + tq];
+      if (M.valid) spec[spec_index(a, M.row, M.reflect ? n - 1 - j : j)] = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+    }
+  }
+}
+
+}  // namespace so3

@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
+#include "dwt_batch.cuh"
 #include "fft.cuh"
 #include "direct.cuh"
 
@@ -142,6 +143,7 @@ struct so3_plan_s {
   int ana_cta = 1;    // analysis: single-CTA 32-degree-tile kernel (SO3_ANA_CTA=0: 2-CTA cluster kernel)
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
+  int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
 };
 
 // ------------------------------------------------------------------ launches
@@ -344,6 +346,24 @@ int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, in
   return launch_dwt_mma_wpc<JW, 1>(analysis, a, warps, ncl, batch, st);
 }
 
+template <int FC, int MTMAX>
+int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+  const dim3 grid(ncl, (batch + FC - 1) / FC);
+  if (analysis) {
+    const size_t smem = so3::batch_analysis_smem<FC>(n);
+    auto k = so3::dwt_analysis_batch_kernel<FC, MTMAX / 4>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, FC * 32, smem, st>>>(a, batch);
+  } else {
+    const size_t smem = so3::batch_synthesis_smem<FC>(n);
+    auto k = so3::dwt_synthesis_batch_kernel<FC, MTMAX>;
+    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, FC * 32, smem, st>>>(a, batch);
+  }
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 template <bool ANALYSIS>
 int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st) {
   if (c0 < 0 || c1 > p->nclusters || c0 > c1)
@@ -368,6 +388,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.J = p->sharded ? p->J : p->n;
   a.slab_stride = p->sharded ? (long long)p->pairs_rank * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
+  if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
+    return launch_dwt_batch<8, 8>(ANALYSIS, a, p->n, ncl, p->batch, st);
   const int syn_jw = p->syn_jw ? p->syn_jw : (p->n == 512 ? 64 : 0);
   if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && syn_jw && (p->n + syn_jw - 1) / syn_jw <= 16) {
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
@@ -694,6 +716,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "ana_cta") { p->ana_cta = value; return SO3_OK; }
   if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
+  if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 

@@ -324,6 +324,43 @@ def test_batch_b32x64_matches_single_function_path():
         assert rel_of_max(gn[f], O.ifsoft(cs[f], b)) < 1e-12
 
 
+@pytest.mark.parametrize("b,F", [(32, 10), (32, 64), (5, 3), (2, 9), (17, 2), (64, 3)])
+def test_batched_dwt_kernels_match_single_function_path(b, F):
+    """Dense-contraction DWT kernels (batched plans, 2B <= 64): ragged function counts
+    (remainder CTAs), padded beta columns (odd B); B=64 batches take the general kernels.  The
+    synthesis is bit-identical to the single-function kernels; the analysis sums beta in a
+    different order, so it is compared to rounding and against the oracle."""
+    C = O.n_coeffs(b)
+    rng = np.random.default_rng(900 + b)
+    cs = rng.standard_normal((F, C)) + 1j * rng.standard_normal((F, C))
+    bplan = plan_for(b, batch=F)
+    grids = so3.ifsoft_batch(torch.from_numpy(cs).cuda(), bplan)
+    back = so3.fsoft_batch(grids, bplan).cpu().numpy()
+    assert np.abs(back - cs).max() < 1e-11
+    single = plan_for(b)
+    gn = grids.cpu().numpy()
+    for f in sorted({0, F // 2, F - 1}):
+        one = so3.ifsoft_sequential(so3.So3Coefficients(b, cs[f]), single).data
+        np.testing.assert_array_equal(one, gn[f])
+        fwd = so3.fsoft_sequential(so3.So3SampleGrid(b, gn[f]), single).data
+        assert rel_of_max(back[f], fwd) < 1e-13
+    if b <= 32:
+        assert rel_of_max(gn[F - 1], O.ifsoft(cs[F - 1], b)) < 1e-12
+        assert rel_of_max(back[0], O.fsoft(gn[0], b)) < 1e-12
+
+
+def test_batched_dwt_knob_off_matches():
+    b, F = 16, 8
+    rng = np.random.default_rng(77)
+    cs = torch.from_numpy(rng.standard_normal((F, O.n_coeffs(b))) + 1j * rng.standard_normal((F, O.n_coeffs(b)))).cuda()
+    p1 = plan_for(b, batch=F)
+    p0 = plan_for(b, batch=F)
+    p0.set_knob("dwt_batch", 0)
+    g1, g0 = so3.ifsoft_batch(cs, p1), so3.ifsoft_batch(cs, p0)
+    assert torch.equal(g1, g0)
+    assert rel_of_max(so3.fsoft_batch(g1, p1).cpu().numpy(), so3.fsoft_batch(g0, p0).cpu().numpy()) < 1e-13
+
+
 def test_sofc_round_trip_through_transform(tmp_path):
     b = 8
     rng = np.random.default_rng(4)

@@ -9,10 +9,11 @@ b = int(sys.argv[1])
 configs = [dict(kv.split("=") for kv in c.split(",")) if c else {} for c in sys.argv[2:]] or [{}]
 n = 2 * b
 C = so3.coeff_count(b)
-plan = so3.make_plan(b)
+F = int(os.environ.get("AB_BATCH", "1"))
+plan = so3.make_plan(b, batch=F)
 rng = np.random.default_rng(b)
-coef = torch.from_numpy(rng.standard_normal(C) + 1j * rng.standard_normal(C)).cuda()
-grid = torch.empty(n ** 3, dtype=torch.complex128, device="cuda")
+coef = torch.from_numpy(rng.standard_normal(F * C) + 1j * rng.standard_normal(F * C)).cuda()
+grid = torch.empty(F * n ** 3, dtype=torch.complex128, device="cuda")
 spec = torch.empty_like(grid)
 out = torch.empty_like(coef)
 stages = {
@@ -22,7 +23,7 @@ stages = {
     "dwt_analysis": lambda: so3.dwt_analysis(plan, spec, out),
 }
 res = {i: {s: [] for s in stages} for i in range(len(configs))}
-defaults = {"dwt_variant": 0, "ana_cta": 1, "syn_jw": 0, "fft_xb": 0}
+defaults = {"dwt_variant": 0, "ana_cta": 1, "syn_jw": 0, "fft_xb": 0, "dwt_batch": 1}
 for rep in range(int(os.environ.get("AB_REPS", "7"))):
     for i, cfg in enumerate(configs):
         for k, v in defaults.items():
@@ -34,4 +35,4 @@ for rep in range(int(os.environ.get("AB_REPS", "7"))):
             if rep > 0:
                 res[i][s].append(e0.elapsed_time(e1))
 for i, cfg in enumerate(configs):
-    print(json.dumps({"B": b, "config": cfg, **{s: round(statistics.median(v), 4) for s, v in res[i].items()}}))
+    print(json.dumps({"B": b, "batch": F, "config": cfg, **{s: round(statistics.median(v), 4) for s, v in res[i].items()}}))

@@ -8,10 +8,11 @@ b = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 n = 2 * b
 C = b * (4 * b * b - 1) // 3
-plan = so3.make_plan(b)
+F = int(os.environ.get("PROF_BATCH", "1"))
+plan = so3.make_plan(b, batch=F)
 rng = np.random.default_rng(b)
-c = torch.from_numpy(rng.standard_normal(C) + 1j * rng.standard_normal(C)).cuda()
-grid = torch.empty(n ** 3, dtype=torch.complex128, device="cuda")
+c = torch.from_numpy(rng.standard_normal(F * C) + 1j * rng.standard_normal(F * C)).cuda()
+grid = torch.empty(F * n ** 3, dtype=torch.complex128, device="cuda")
 spec = torch.empty_like(grid)
 out = torch.empty_like(c)
 for _ in range(steps):
