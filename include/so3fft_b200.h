@@ -141,28 +141,42 @@ void* so3_plan_scratch(so3_plan_t plan);
 
 /* ---- sharded pipeline (one process per GPU) -------------------
  * G ranks split the torus FFT by beta slab [rank*J, (rank+1)*J), J = 2B/G, and the DWT by
- * cost-balanced cluster groups (longest-processing-time greedy over the schedule); one
+ * cost-balanced cluster groups (longest-processing-time greedy over the schedule); an
  * all-to-all per direction joins them (the reference's in-memory transpose spectrum[m, j, m'],
- * soft.py:131-132, 142, 167).  Buffers (complex128):
+ * soft.py:131-132, 142, 167).  The exchange is split into K chunks: each rank's cost-sorted
+ * cluster list is cut into K runs of equal DWT cost, and every layout is chunk-major so one
+ * chunk is one contiguous all-to-all (its exchange overlaps the DWT of the previous / next
+ * chunk).  Buffers (complex128):
  *   slab     : [i][jj][k], 2B x J x 2B (this rank's samples; grid[:, jbase:jbase+J, :])
- *   layout A : rows [rank g][pairs_g][J]   (forward send / inverse recv, total (2B-1)^2 * J)
- *   layout B : rows [rank h][pairs_rank][J] (forward recv / inverse send, G * pairs_rank * J)
+ *   layout A : rows [chunk q][rank g][pairs_{g,q}][J]  (forward send / inverse recv,
+ *              total (2B-1)^2 * J)
+ *   layout B : rows [chunk q][rank h][pairs_{rank,q}][J] (forward recv / inverse send,
+ *              G * pairs_rank * J); chunk q starts at row G * sum_{q' < q} pairs_{rank,q'}
  *   coeffs   : full l-major array; a rank writes (forward) / reads (inverse) only its slots.
- * Results are identical, bit for bit, for every G (the same per-row FFTs and per-cluster
- * reductions run whatever the split). */
-int so3_shard_plan_create(int bandwidth, int world, int rank, so3_plan_t* out);
+ * Results are identical, bit for bit, for every G and K (the same per-row FFTs and
+ * per-cluster reductions run whatever the split).  K = 1 is the unchunked exchange. */
+int so3_shard_plan_create(int bandwidth, int world, int rank, so3_plan_t* out);      /* K = 1 */
+int so3_shard_plan_create_chunked(int bandwidth, int world, int rank, int chunks, so3_plan_t* out);
 int64_t so3_shard_slab_width(so3_plan_t plan);             /* J */
 int64_t so3_shard_rank_pairs(so3_plan_t plan);             /* pairs_rank */
-/* host only: pairs per rank [world]; cluster owner per schedule entry; a rank's pairs (m, m') */
+int64_t so3_shard_chunks(so3_plan_t plan);                 /* K */
+/* host only: pairs per rank [world]; cluster owner per schedule entry; a rank's pairs (m, m')
+ * in layout order (chunk by chunk); pairs per (chunk, rank) [chunks][world] */
 int so3_shard_pair_counts(int bandwidth, int world, int64_t* pairs_per_rank);
 int so3_shard_cluster_owner(int bandwidth, int world, int32_t* owner);
 int so3_shard_pair_list(int bandwidth, int world, int rank, int32_t* pairs);
+int so3_shard_chunk_pairs(int bandwidth, int world, int chunks, int64_t* pairs);
 /* forward: slab -> layout A (K1a + K1b with the pack fused into the store) */
 int so3_shard_fft_analysis(so3_plan_t plan, const void* slab_dev, void* send_dev, void* stream);
 /* forward: layout B -> this rank's coefficient slots */
 int so3_shard_dwt_analysis(so3_plan_t plan, const void* recv_dev, void* coeffs_dev, void* stream);
 /* inverse: this rank's coefficient slots -> layout B */
 int so3_shard_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* send_dev, void* stream);
+/* one chunk q: recv_chunk / send_chunk point at chunk q of layout B ([h][pairs_{rank,q}][J]) */
+int so3_shard_dwt_analysis_chunk(so3_plan_t plan, int chunk, const void* recv_chunk_dev, void* coeffs_dev,
+                                 void* stream);
+int so3_shard_dwt_synthesis_chunk(so3_plan_t plan, int chunk, const void* coeffs_dev, void* send_chunk_dev,
+                                  void* stream);
 /* inverse: layout A -> slab (K4a with the unpack fused into the load, K4b) */
 int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_dev, void* stream);
 

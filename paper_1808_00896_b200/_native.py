@@ -56,6 +56,11 @@ SIGNATURES = {
     "so3_fsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),
     "so3_ifsoft_direct": (_c_int, [_c_int, _vp, _vp, _vp]),
     "so3_shard_plan_create": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
+    "so3_shard_plan_create_chunked": (_c_int, [_c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_vp)]),
+    "so3_shard_chunks": (_c_i64, [_vp]),
+    "so3_shard_chunk_pairs": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(_c_i64)]),
+    "so3_shard_dwt_analysis_chunk": (_c_int, [_vp, _c_int, _vp, _vp, _vp]),
+    "so3_shard_dwt_synthesis_chunk": (_c_int, [_vp, _c_int, _vp, _vp, _vp]),
     "so3_shard_slab_width": (_c_i64, [_vp]),
     "so3_shard_rank_pairs": (_c_i64, [_vp]),
     "so3_shard_pair_counts": (_c_int, [_c_int, _c_int, ctypes.POINTER(_c_i64)]),

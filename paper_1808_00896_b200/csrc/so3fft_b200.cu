@@ -95,6 +95,22 @@ std::vector<int> shard_owner(const std::vector<Cluster>& cl, int b, int world) {
   return owner;
 }
 
+// Exchange chunks of the sharded pipeline: each rank's cost-sorted cluster list is cut into
+// `chunks` contiguous runs of (nearly) equal DWT cost, so the all-to-all of chunk q+1 can
+// overlap the DWT of chunk q.  chunk_of[i] for schedule entry i (its owner's run).
+std::vector<int> shard_chunks(const std::vector<Cluster>& cl, const std::vector<int>& owner, int b, int world,
+                              int chunks) {
+  std::vector<long long> total(world, 0), seen(world, 0);
+  for (size_t i = 0; i < cl.size(); ++i) total[owner[i]] += (long long)cl[i].members * (b - cl[i].m) + 1;
+  std::vector<int> chunk_of(cl.size());
+  for (size_t i = 0; i < cl.size(); ++i) {
+    const int r = owner[i];
+    chunk_of[i] = (int)std::min<long long>(chunks - 1, seen[r] * chunks / std::max<long long>(total[r], 1));
+    seen[r] += (long long)cl[i].members * (b - cl[i].m) + 1;
+  }
+  return chunk_of;
+}
+
 // Member order pairs of a base pair in tag order (schedule.py:115-133), as make_member.
 std::vector<std::pair<int, int>> cluster_pairs(int m, int mp) {
   static const int rel[8][4] = {{1, 0, 0, 1}, {-1, 0, 0, -1}, {0, 1, 1, 0}, {0, -1, -1, 0},
@@ -138,7 +154,11 @@ struct so3_plan_s {
   int64_t pairs_rank = 0;               // order pairs owned by this rank (DWT rows)
   std::vector<int64_t> pairs_of;        // pairs per rank
   int* d_row_global = nullptr;          // (m' bin)*n + (m bin) -> row of layout [rank g][pairs_g][J], -1 if none
-  int* d_row_local = nullptr;           // same index -> row among this rank's pairs, -1 if not owned
+  int* d_row_local = nullptr;           // same index -> row among this rank's pairs of its chunk, -1 if not owned
+  int chunks = 1;                       // exchange chunks (layouts are chunk-major, see the header)
+  std::vector<int64_t> chunk_cl;        // this rank's clusters of chunk q: [chunk_cl[q], chunk_cl[q+1])
+  std::vector<int64_t> chunk_pairs;     // this rank's pairs of chunk q
+  std::vector<int64_t> chunk_off;       // prefix of chunk_pairs
   int dwt_variant = SO3_DWT_MMA;
   int ana_cta = 1;    // analysis: single-CTA 32-degree-tile kernel (SO3_ANA_CTA=0: 2-CTA cluster kernel)
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
@@ -365,7 +385,8 @@ int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, 
 }
 
 template <bool ANALYSIS>
-int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st) {
+int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st,
+               int64_t chunk_pairs = -1) {
   if (c0 < 0 || c1 > p->nclusters || c0 > c1)
     return fail(SO3_ERR_INVALID, "cluster range [" + std::to_string(c0) + ", " + std::to_string(c1) +
                                      ") outside [0, " + std::to_string(p->nclusters) + ")");
@@ -386,7 +407,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.rc_off = p->d_rc_off;
   a.rowtab = p->sharded ? p->d_row_local : nullptr;
   a.J = p->sharded ? p->J : p->n;
-  a.slab_stride = p->sharded ? (long long)p->pairs_rank * p->J : 0;
+  // sharded: spec is one chunk [h][pairs_chunk][J] of layout B (chunk_pairs; default = all pairs)
+  a.slab_stride = p->sharded ? (long long)(chunk_pairs >= 0 ? chunk_pairs : p->pairs_rank) * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch<8, 8>(ANALYSIS, a, p->n, ncl, p->batch, st);
@@ -602,38 +624,60 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
 }
 
 int so3_shard_plan_create(int b, int world, int rank, so3_plan_t* out) {
+  return so3_shard_plan_create_chunked(b, world, rank, 1, out);
+}
+
+int so3_shard_plan_create_chunked(int b, int world, int rank, int chunks, so3_plan_t* out) {
   if (!out) return fail(SO3_ERR_INVALID, "null plan output");
   *out = nullptr;
   if (!valid_bandwidth(b) || b > 1024) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 1024], got " + std::to_string(b));
   if (world < 1 || rank < 0 || rank >= world) return fail(SO3_ERR_INVALID, "rank outside [0, world)");
   if ((2 * b) % world) return fail(SO3_ERR_INVALID, "2B must be divisible by the number of ranks");
+  if (chunks < 1 || chunks > 64) return fail(SO3_ERR_INVALID, "chunks must be in [1, 64]");
   so3_plan_s* p = new_plan(b, 1);
   p->sharded = 1;
   p->world = world;
   p->rank = rank;
   p->J = p->n / world;
   p->jbase = rank * p->J;
+  p->chunks = chunks;
   const int n = p->n;
   const auto all = host_clusters(b);
   const auto owner = shard_owner(all, b, world);
-  std::vector<Cluster> mine;
+  const auto chunk_of = shard_chunks(all, owner, b, world, chunks);
+  // pairs per (chunk, rank); layout A rows are [q][g][pairs_{g,q}], layout B rows [q][h][pairs_{rank,q}]
+  std::vector<int64_t> cnt((size_t)chunks * world, 0);
   p->pairs_of.assign(world, 0);
-  std::vector<int> row_global((size_t)n * n, -1), row_local((size_t)n * n, -1);
-  std::vector<int64_t> prefix(world + 1, 0);
-  for (size_t i = 0; i < all.size(); ++i) p->pairs_of[owner[i]] += all[i].members;
-  for (int r = 0; r < world; ++r) prefix[r + 1] = prefix[r] + p->pairs_of[r];
-  std::vector<int64_t> next(world, 0);
   for (size_t i = 0; i < all.size(); ++i) {
-    const int r = owner[i];
-    if (r == rank) mine.push_back(all[i]);
+    cnt[(size_t)chunk_of[i] * world + owner[i]] += all[i].members;
+    p->pairs_of[owner[i]] += all[i].members;
+  }
+  std::vector<int64_t> base_a((size_t)chunks * world + 1, 0);
+  for (size_t k = 0; k < cnt.size(); ++k) base_a[k + 1] = base_a[k] + cnt[k];
+  std::vector<int64_t> next((size_t)chunks * world, 0);
+  std::vector<int> row_global((size_t)n * n, -1), row_local((size_t)n * n, -1);
+  std::vector<Cluster> mine;
+  p->chunk_cl.assign(chunks + 1, 0);
+  p->chunk_pairs.assign(chunks, 0);
+  for (size_t i = 0; i < all.size(); ++i) {
+    const int r = owner[i], q = chunk_of[i];
+    const size_t k = (size_t)q * world + r;
+    if (r == rank) {
+      mine.push_back(all[i]);
+      p->chunk_cl[q + 1] = (int64_t)mine.size();
+      p->chunk_pairs[q] += all[i].members;
+    }
     for (const auto& pr : cluster_pairs(all[i].m, all[i].mp)) {
       const int bm = ((pr.first % n) + n) % n, bmp = ((pr.second % n) + n) % n;
       const size_t idx = (size_t)bmp * n + bm;
-      row_global[idx] = (int)(prefix[r] + next[r]);
-      if (r == rank) row_local[idx] = (int)next[r];
-      ++next[r];
+      row_global[idx] = (int)(base_a[k] + next[k]);
+      if (r == rank) row_local[idx] = (int)next[k];
+      ++next[k];
     }
   }
+  for (int q = 1; q <= chunks; ++q) p->chunk_cl[q] = std::max(p->chunk_cl[q], p->chunk_cl[q - 1]);
+  p->chunk_off.assign(chunks + 1, 0);
+  for (int q = 0; q < chunks; ++q) p->chunk_off[q + 1] = p->chunk_off[q] + p->chunk_pairs[q];
   p->pairs_rank = p->pairs_of[rank];
   int rc = build_plan(p, mine);
   if (rc) { so3_plan_destroy(p); return rc; }
@@ -646,6 +690,18 @@ int so3_shard_plan_create(int b, int world, int rank, so3_plan_t* out) {
   *out = p;
   return SO3_OK;
 }
+
+int so3_shard_chunk_pairs(int b, int world, int chunks, int64_t* pairs) {
+  if (!valid_bandwidth(b) || world < 1 || chunks < 1 || chunks > 64 || !pairs) return fail(SO3_ERR_INVALID, "bad arguments");
+  const auto all = host_clusters(b);
+  const auto owner = shard_owner(all, b, world);
+  const auto chunk_of = shard_chunks(all, owner, b, world, chunks);
+  for (int k = 0; k < chunks * world; ++k) pairs[k] = 0;
+  for (size_t i = 0; i < all.size(); ++i) pairs[(size_t)chunk_of[i] * world + owner[i]] += all[i].members;
+  return SO3_OK;
+}
+
+int64_t so3_shard_chunks(so3_plan_t p) { return p ? p->chunks : 0; }
 
 int so3_shard_pair_counts(int b, int world, int64_t* pairs_per_rank) {
   if (!valid_bandwidth(b) || world < 1 || !pairs_per_rank) return fail(SO3_ERR_INVALID, "bad arguments");
@@ -832,14 +888,38 @@ int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* str
   return launch_fft(shard_pass_args(p, 1, p->d_scratch, send), +1, 1, st, p->fft_wide);
 }
 
+#define CHECK_CHUNK(p, q) \
+  if ((q) < 0 || (q) >= (p)->chunks) return fail(SO3_ERR_INVALID, "chunk outside [0, chunks)")
+
+// chunk q of layout B starts at row world * chunk_off[q]
+int so3_shard_dwt_analysis_chunk(so3_plan_t p, int q, const void* recv_chunk, void* coeffs, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_CHUNK(p, q); CHECK_PTR(recv_chunk); CHECK_PTR(coeffs);
+  return launch_dwt<true>(p, recv_chunk, coeffs, p->chunk_cl[q], p->chunk_cl[q + 1], static_cast<cudaStream_t>(stream),
+                          p->chunk_pairs[q]);
+}
+
+int so3_shard_dwt_synthesis_chunk(so3_plan_t p, int q, const void* coeffs, void* send_chunk, void* stream) {
+  CHECK_PLAN(p); CHECK_SHARD(p); CHECK_CHUNK(p, q); CHECK_PTR(coeffs); CHECK_PTR(send_chunk);
+  return launch_dwt<false>(p, send_chunk, const_cast<void*>(coeffs), p->chunk_cl[q], p->chunk_cl[q + 1],
+                           static_cast<cudaStream_t>(stream), p->chunk_pairs[q]);
+}
+
 int so3_shard_dwt_analysis(so3_plan_t p, const void* recv, void* coeffs, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(recv); CHECK_PTR(coeffs);
-  return launch_dwt<true>(p, recv, coeffs, 0, p->nclusters, static_cast<cudaStream_t>(stream));
+  for (int q = 0; q < p->chunks; ++q) {
+    const double2* part = static_cast<const double2*>(recv) + (int64_t)p->world * p->chunk_off[q] * p->J;
+    if (int rc = so3_shard_dwt_analysis_chunk(p, q, part, coeffs, stream)) return rc;
+  }
+  return SO3_OK;
 }
 
 int so3_shard_dwt_synthesis(so3_plan_t p, const void* coeffs, void* send, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(coeffs); CHECK_PTR(send);
-  return launch_dwt<false>(p, send, const_cast<void*>(coeffs), 0, p->nclusters, static_cast<cudaStream_t>(stream));
+  for (int q = 0; q < p->chunks; ++q) {
+    double2* part = static_cast<double2*>(send) + (int64_t)p->world * p->chunk_off[q] * p->J;
+    if (int rc = so3_shard_dwt_synthesis_chunk(p, q, coeffs, part, stream)) return rc;
+  }
+  return SO3_OK;
 }
 
 int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* stream) {

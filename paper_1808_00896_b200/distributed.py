@@ -9,15 +9,18 @@ G ranks split
   * the DWT by cost-balanced symmetry-cluster groups (LPT greedy over the launch schedule,
     computed by the C library: so3_shard_*);
 
-and the transpose becomes one ``torch.distributed.all_to_all_single`` (NCCL over NVLink on a
-B200 box, gloo in the CPU tests).  Pack and unpack are fused into the FFT kernels through a
-pair -> row table, so the exchange moves the FFT output / DWT output buffers directly:
+and the transpose becomes ``torch.distributed.all_to_all_single`` (NCCL over NVLink on a
+B200 box, gloo in the CPU tests), split into K chunks of clusters so the exchange overlaps
+the DWT: forward, the all-to-alls of all chunks are queued behind the FFT and the DWT of
+chunk q starts as soon as chunk q has arrived; inverse, chunk q is sent while chunk q+1 is
+synthesised.  Pack and unpack are fused into the FFT kernels through a pair -> row table,
+so the exchange moves the FFT output / DWT output buffers directly:
 
-  layout A  rows [rank g][pairs_g][J]      forward send, inverse recv
-  layout B  rows [rank h][pairs_rank][J]   forward recv, inverse send
+  layout A  rows [chunk q][rank g][pairs_{g,q}][J]      forward send, inverse recv
+  layout B  rows [chunk q][rank h][pairs_{rank,q}][J]   forward recv, inverse send
 
-Results are bit-identical for every G (the same per-row FFTs and per-cluster reductions run
-whatever the split).  Coefficients stay sharded: a rank writes / reads only the slots of its
+Results are bit-identical for every G and K (the same per-row FFTs and per-cluster
+reductions run whatever the split).  Coefficients stay sharded: a rank writes / reads only the slots of its
 clusters in a full-length array; ``gather_coefficients`` all-reduces them (each slot has one
 writer and zeros elsewhere, so the sum is exact).
 
@@ -36,20 +39,29 @@ from .core import coeff_count, grid_size, validate_bandwidth
 
 
 class ShardMap:
-    """Host-side shard map of G ranks (no GPU needed): pairs per rank, slab width, splits."""
+    """Host-side shard map of G ranks and K exchange chunks (no GPU needed): pairs per
+    (chunk, rank), slab width, all-to-all splits and buffer offsets."""
 
-    def __init__(self, bandwidth: int, world: int):
+    def __init__(self, bandwidth: int, world: int, chunks: int = 1):
         self.bandwidth = validate_bandwidth(bandwidth)
         n = grid_size(self.bandwidth)
         if world < 1 or n % world:
             raise ValueError(f"2B={n} must be divisible by the number of ranks {world}")
+        if not 1 <= chunks <= 64:
+            raise ValueError(f"chunks must be in [1, 64], got {chunks}")
         self.world = world
+        self.chunks = chunks
         self.n = n
         self.J = n // world
         counts = (ctypes.c_int64 * world)()
         _native.check(_native.lib().so3_shard_pair_counts(self.bandwidth, world, counts), "shard_pair_counts")
         self.pairs = [int(v) for v in counts]
         assert sum(self.pairs) == (n - 1) ** 2
+        cp = (ctypes.c_int64 * (chunks * world))()
+        _native.check(_native.lib().so3_shard_chunk_pairs(self.bandwidth, world, chunks, cp), "shard_chunk_pairs")
+        # chunk_pairs[q][g]: pairs of rank g in chunk q
+        self.chunk_pairs = [[int(cp[q * world + g]) for g in range(world)] for q in range(chunks)]
+        assert [sum(self.chunk_pairs[q][g] for q in range(chunks)) for g in range(world)] == self.pairs
 
     def pair_list(self, rank: int) -> np.ndarray:
         out = np.empty((self.pairs[rank], 2), dtype=np.int32)
@@ -70,26 +82,38 @@ class ShardMap:
     def layout_b_rows(self, rank: int) -> int:
         return self.world * self.pairs[rank]
 
-    # all_to_all_single split sizes, in complex128 elements
-    def forward_send_splits(self, rank: int) -> list[int]:
-        return [p * self.J for p in self.pairs]
+    # element ranges of chunk q (complex128 units)
+    def chunk_a(self, q: int) -> tuple[int, int]:
+        start = sum(sum(self.chunk_pairs[p]) for p in range(q)) * self.J
+        return start, start + sum(self.chunk_pairs[q]) * self.J
 
-    def forward_recv_splits(self, rank: int) -> list[int]:
-        return [self.pairs[rank] * self.J] * self.world
+    def chunk_b(self, rank: int, q: int) -> tuple[int, int]:
+        start = self.world * sum(self.chunk_pairs[p][rank] for p in range(q)) * self.J
+        return start, start + self.world * self.chunk_pairs[q][rank] * self.J
 
-    def inverse_send_splits(self, rank: int) -> list[int]:
-        return self.forward_recv_splits(rank)
+    # all_to_all_single split sizes of chunk q, in complex128 elements
+    def forward_send_splits(self, rank: int, q: int = 0) -> list[int]:
+        if self.chunks == 1:
+            return [p * self.J for p in self.pairs]
+        return [p * self.J for p in self.chunk_pairs[q]]
 
-    def inverse_recv_splits(self, rank: int) -> list[int]:
-        return self.forward_send_splits(rank)
+    def forward_recv_splits(self, rank: int, q: int = 0) -> list[int]:
+        own = self.pairs[rank] if self.chunks == 1 else self.chunk_pairs[q][rank]
+        return [own * self.J] * self.world
+
+    def inverse_send_splits(self, rank: int, q: int = 0) -> list[int]:
+        return self.forward_recv_splits(rank, q)
+
+    def inverse_recv_splits(self, rank: int, q: int = 0) -> list[int]:
+        return self.forward_send_splits(rank, q)
 
 
 class ShardBackend(Protocol):
     """The four stage kernels of one rank (buffer layouts above)."""
 
     def fft_analysis(self, slab, send_a) -> None: ...
-    def dwt_analysis(self, recv_b, coeffs) -> None: ...
-    def dwt_synthesis(self, coeffs, send_b) -> None: ...
+    def dwt_analysis_chunk(self, q, recv_b_chunk, coeffs) -> None: ...
+    def dwt_synthesis_chunk(self, q, coeffs, send_b_chunk) -> None: ...
     def fft_synthesis(self, recv_a, slab) -> None: ...
     def empty(self, count: int): ...
     def zeros(self, count: int): ...
@@ -98,16 +122,17 @@ class ShardBackend(Protocol):
 class NativeShardBackend:
     """CUDA kernels of libso3fft_b200.so on the current device (torch complex128 tensors)."""
 
-    def __init__(self, bandwidth: int, world: int, rank: int, device=None):
+    def __init__(self, bandwidth: int, world: int, rank: int, device=None, chunks: int = 1):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
         handle = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             torch.empty(1, device=self.device)
-            _native.check(_native.lib().so3_shard_plan_create(bandwidth, world, rank, ctypes.byref(handle)),
-                          "shard_plan_create")
+            _native.check(_native.lib().so3_shard_plan_create_chunked(bandwidth, world, rank, chunks,
+                                                                      ctypes.byref(handle)), "shard_plan_create")
         self.handle = handle
+        self.chunks = chunks
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -127,6 +152,14 @@ class NativeShardBackend:
     def dwt_synthesis(self, coeffs, send_b):
         _native.check(_native.lib().so3_shard_dwt_synthesis(self.handle, self._p(coeffs), self._p(send_b), self._stream()),
                       "shard_dwt_synthesis")
+
+    def dwt_analysis_chunk(self, q, recv_chunk, coeffs):
+        _native.check(_native.lib().so3_shard_dwt_analysis_chunk(self.handle, q, self._p(recv_chunk), self._p(coeffs),
+                                                                  self._stream()), "shard_dwt_analysis_chunk")
+
+    def dwt_synthesis_chunk(self, q, coeffs, send_chunk):
+        _native.check(_native.lib().so3_shard_dwt_synthesis_chunk(self.handle, q, self._p(coeffs), self._p(send_chunk),
+                                                                   self._stream()), "shard_dwt_synthesis_chunk")
 
     def fft_synthesis(self, recv_a, slab):
         _native.check(_native.lib().so3_shard_fft_synthesis(self.handle, self._p(recv_a), self._p(slab), self._stream()),
@@ -156,44 +189,67 @@ def _as_real(t):
 
 
 class ShardedSO3:
-    """One rank of the sharded transform pair.  ``exchange`` defaults to all_to_all_single."""
+    """One rank of the sharded transform pair.  The backend's chunk count K (default 1) sets
+    the pipelining of the exchange (see the module docstring)."""
 
-    def __init__(self, bandwidth: int, rank: int, world: int, backend: ShardBackend, group=None):
-        self.map = ShardMap(bandwidth, world)
+    def __init__(self, bandwidth: int, rank: int, world: int, backend: ShardBackend, group=None, chunks=None):
+        chunks = getattr(backend, "chunks", 1) if chunks is None else chunks
+        self.map = ShardMap(bandwidth, world, chunks)
         self.bandwidth = self.map.bandwidth
-        self.rank, self.world = rank, world
+        self.rank, self.world, self.chunks = rank, world, chunks
         self.backend = backend
         self.group = group
         self.coeff_count = coeff_count(self.bandwidth)
         self.slab_count = self.map.n * self.map.J * self.map.n
 
-    def _all_to_all(self, recv, send, recv_splits, send_splits):
+    def _all_to_all(self, recv, send, recv_splits, send_splits, async_op=False):
         import torch.distributed as dist
         if self.world == 1:
             recv.copy_(send)
-            return
-        dist.all_to_all_single(_as_real(recv), _as_real(send),
-                               output_split_sizes=[2 * s for s in recv_splits],
-                               input_split_sizes=[2 * s for s in send_splits], group=self.group)
+            return None
+        return dist.all_to_all_single(_as_real(recv), _as_real(send),
+                                      output_split_sizes=[2 * s for s in recv_splits],
+                                      input_split_sizes=[2 * s for s in send_splits], group=self.group,
+                                      async_op=async_op)
 
     def fsoft(self, slab):
-        """This rank's beta slab [i][jj][k] -> coefficients (own slots; others zero)."""
-        m = self.map
+        """This rank's beta slab [i][jj][k] -> coefficients (own slots; others zero).
+        All chunk exchanges are queued behind the FFT; the DWT of chunk q waits for chunk q
+        only (on the device stream for NCCL), so it overlaps the exchange of chunks > q."""
+        m, r = self.map, self.rank
         send = self.backend.empty(m.layout_a_rows() * m.J)
         self.backend.fft_analysis(slab, send)
-        recv = self.backend.empty(m.layout_b_rows(self.rank) * m.J)
-        self._all_to_all(recv, send, m.forward_recv_splits(self.rank), m.forward_send_splits(self.rank))
+        recv = self.backend.empty(m.layout_b_rows(r) * m.J)
+        works = []
+        for q in range(self.chunks):
+            a0, a1 = m.chunk_a(q)
+            b0, b1 = m.chunk_b(r, q)
+            works.append(self._all_to_all(recv[b0:b1], send[a0:a1], m.forward_recv_splits(r, q),
+                                          m.forward_send_splits(r, q), async_op=True))
         coeffs = self.backend.zeros(self.coeff_count)
-        self.backend.dwt_analysis(recv, coeffs)
+        for q in range(self.chunks):
+            if works[q] is not None:
+                works[q].wait()
+            b0, b1 = m.chunk_b(r, q)
+            self.backend.dwt_analysis_chunk(q, recv[b0:b1], coeffs)
         return coeffs
 
     def ifsoft(self, coeffs):
-        """Coefficients (this rank's slots are read) -> this rank's beta slab [i][jj][k]."""
-        m = self.map
-        send = self.backend.empty(m.layout_b_rows(self.rank) * m.J)
-        self.backend.dwt_synthesis(coeffs, send)
+        """Coefficients (this rank's slots are read) -> this rank's beta slab [i][jj][k].
+        Chunk q is exchanged while chunk q+1 is synthesised."""
+        m, r = self.map, self.rank
+        send = self.backend.empty(m.layout_b_rows(r) * m.J)
         recv = self.backend.empty(m.layout_a_rows() * m.J)
-        self._all_to_all(recv, send, m.inverse_recv_splits(self.rank), m.inverse_send_splits(self.rank))
+        works = []
+        for q in range(self.chunks):
+            b0, b1 = m.chunk_b(r, q)
+            a0, a1 = m.chunk_a(q)
+            self.backend.dwt_synthesis_chunk(q, coeffs, send[b0:b1])
+            works.append(self._all_to_all(recv[a0:a1], send[b0:b1], m.inverse_recv_splits(r, q),
+                                          m.inverse_send_splits(r, q), async_op=True))
+        for w in works:
+            if w is not None:
+                w.wait()
         slab = self.backend.empty(self.slab_count)
         self.backend.fft_synthesis(recv, slab)
         return slab

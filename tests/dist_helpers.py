@@ -1,7 +1,7 @@
 """Numpy stand-in for the four sharded stage kernels (test infrastructure: lets the gloo
 tests run the real shard map + exchange orchestration of paper_1808_00896_b200.distributed
 on CPU).  Layouts follow include/so3fft_b200.h: slab [i][jj][k], layout A rows
-[g][pairs_g][J], layout B rows [h][pairs_rank][J]."""
+[q][g][pairs_{g,q}][J], layout B rows [q][h][pairs_{rank,q}][J] (chunk-major)."""
 import math
 
 import numpy as np
@@ -13,22 +13,33 @@ from paper_1808_00896_b200.distributed import ShardMap
 
 
 class NumpyShardBackend:
-    def __init__(self, b: int, world: int, rank: int):
-        self.b, self.world, self.rank = b, world, rank
-        self.map = ShardMap(b, world)
+    def __init__(self, b: int, world: int, rank: int, chunks: int = 1):
+        self.b, self.world, self.rank, self.chunks = b, world, rank, chunks
+        self.map = ShardMap(b, world, chunks)
         self.n, self.J = self.map.n, self.map.J
         self.jbase = rank * self.J
-        lists = [self.map.pair_list(g) for g in range(world)]
-        self.glob = {}
-        off = 0
-        for g in range(world):
-            for p, (pm, pmp) in enumerate(lists[g].tolist()):
-                self.glob[(pm, pmp)] = off + p
-            off += len(lists[g])
-        self.local = {tuple(x): p for p, x in enumerate(lists[rank].tolist())}
+        cp = self.map.chunk_pairs
+        lists = [self.map.pair_list(g).tolist() for g in range(world)]   # layout order, chunk by chunk
+        # layout A row of every pair: rows [q][g][pairs_{g,q}]
+        self.glob, self.local = {}, {}
+        row = 0
+        off = [0] * world
+        for q in range(chunks):
+            for g in range(world):
+                for i in range(cp[q][g]):
+                    pair = tuple(lists[g][off[g] + i])
+                    self.glob[pair] = row
+                    row += 1
+                    if g == rank:
+                        self.local[pair] = (q, i)
+                off[g] += cp[q][g]
         bases, _ = cluster_schedule(b)
         owner = self.map.cluster_owner()
-        self.clusters = [tuple(bases[i].tolist()) for i in range(len(bases)) if owner[i] == rank]
+        self.clusters = [[] for _ in range(chunks)]
+        for i in range(len(bases)):
+            if owner[i] == rank:
+                base = tuple(bases[i].tolist())
+                self.clusters[self.local[base][0]].append(base)
         self.betas = O.beta_nodes(b)
         self.w = O.beta_weights(b)
         self.v = (2.0 * np.arange(b) + 1.0) / (8.0 * math.pi * b)
@@ -58,24 +69,24 @@ class NumpyShardBackend:
                 S[pm % n, pmp % n] = a[R * J + jj]
             s[:, jj, :] = O.slice_dft(S, -1)
 
-    def dwt_analysis(self, recv, coeffs):
-        P = len(self.local)
-        r = recv.numpy().reshape(self.world, P, self.J)
+    def dwt_analysis_chunk(self, q, recv_chunk, coeffs):
+        P = self.map.chunk_pairs[q][self.rank]
+        r = recv_chunk.numpy().reshape(self.world, P, self.J)
         c = coeffs.numpy()
         ones = np.ones(self.n)
-        for (bm, bmp) in self.clusters:
+        for (bm, bmp) in self.clusters[q]:
             rows = O.recurrence_rows(bm, bmp, self.betas, self.b)
             for (pm, pmp, tag) in O.cluster_members(bm, bmp):
-                col = r[:, self.local[(pm, pmp)], :].reshape(-1)
+                col = r[:, self.local[(pm, pmp)][1], :].reshape(-1)
                 mat = O.member_matrix(rows, tag, bm, bmp, self.b)
                 c[O.pair_slots(pm, pmp, self.b)] = O.analysis_column(mat, self.v[bm:], ones, col)
 
-    def dwt_synthesis(self, coeffs, send):
-        P = len(self.local)
-        out = send.numpy().reshape(self.world, P, self.J)
+    def dwt_synthesis_chunk(self, q, coeffs, send_chunk):
+        P = self.map.chunk_pairs[q][self.rank]
+        out = send_chunk.numpy().reshape(self.world, P, self.J)
         c = coeffs.numpy()
-        for (bm, bmp) in self.clusters:
+        for (bm, bmp) in self.clusters[q]:
             rows = O.recurrence_rows(bm, bmp, self.betas, self.b)
             for (pm, pmp, tag) in O.cluster_members(bm, bmp):
                 g = O.synthesis_column(O.member_matrix(rows, tag, bm, bmp, self.b), c[O.pair_slots(pm, pmp, self.b)])
-                out[:, self.local[(pm, pmp)], :] = g.reshape(self.world, self.J)
+                out[:, self.local[(pm, pmp)][1], :] = g.reshape(self.world, self.J)

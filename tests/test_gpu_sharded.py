@@ -12,14 +12,14 @@ so3 = pytest.importorskip("paper_1808_00896_b200")
 from paper_1808_00896_b200.distributed import NativeShardBackend, ShardMap  # noqa: E402
 
 
-def emulate(b, world, grid, coeffs):
+def emulate(b, world, grid, coeffs, chunks=1):
     n = 2 * b
-    m = ShardMap(b, world)
+    m = ShardMap(b, world, chunks)
     J = m.J
-    pref = np.concatenate([[0], np.cumsum(m.pairs)])
-    be = [NativeShardBackend(b, world, r) for r in range(world)]
+    cp = m.chunk_pairs
+    be = [NativeShardBackend(b, world, r, chunks=chunks) for r in range(world)]
     cube = grid.reshape(n, n, n)
-    # forward
+    # forward: FFT per slab, then chunk by chunk exchange (device copies) + per-chunk DWT
     sends = []
     for r in range(world):
         slab = cube[:, r * J:(r + 1) * J, :].contiguous().reshape(-1)
@@ -28,19 +28,28 @@ def emulate(b, world, grid, coeffs):
         sends.append(s)
     out = torch.zeros_like(coeffs)
     for g in range(world):
-        recv = torch.cat([sends[h][pref[g] * J:pref[g + 1] * J] for h in range(world)])
         c = be[g].zeros(out.numel())
-        be[g].dwt_analysis(recv, c)
+        for q in range(chunks):
+            a0 = m.chunk_a(q)[0] + sum(cp[q][:g]) * J
+            recv = torch.cat([sends[h][a0:a0 + cp[q][g] * J] for h in range(world)])
+            be[g].dwt_analysis_chunk(q, recv, c)
         out += c
-    # inverse
+    # inverse: per-chunk synthesis into layout B, exchange, FFT per slab
     sends = []
     for g in range(world):
         s = be[g].empty(m.layout_b_rows(g) * J)
-        be[g].dwt_synthesis(coeffs, s)
+        for q in range(chunks):
+            b0, b1 = m.chunk_b(g, q)
+            be[g].dwt_synthesis_chunk(q, coeffs, s[b0:b1])
         sends.append(s)
     slabs = []
     for h in range(world):
-        recv = torch.cat([sends[g][h * m.pairs[g] * J:(h + 1) * m.pairs[g] * J] for g in range(world)])
+        parts = []
+        for q in range(chunks):
+            for g in range(world):
+                b0 = m.chunk_b(g, q)[0] + h * cp[q][g] * J
+                parts.append(sends[g][b0:b0 + cp[q][g] * J])
+        recv = torch.cat(parts)
         slab = be[h].empty(n * J * n)
         be[h].fft_synthesis(recv, slab)
         slabs.append(slab.reshape(n, J, n))
@@ -51,8 +60,9 @@ def emulate(b, world, grid, coeffs):
     return out, back
 
 
-@pytest.mark.parametrize("b,world", [(8, 2), (16, 4), (33, 2), (64, 8), (128, 4)])
-def test_sharded_equals_single_gpu_bitwise(b, world):
+@pytest.mark.parametrize("b,world,chunks", [(8, 2, 1), (16, 4, 1), (33, 2, 1), (64, 8, 1), (128, 4, 1),
+                                            (16, 2, 3), (64, 4, 4), (128, 8, 8), (5, 2, 6)])
+def test_sharded_equals_single_gpu_bitwise(b, world, chunks):
     n = 2 * b
     rng = np.random.default_rng(b + world)
     grid = torch.from_numpy(rng.standard_normal(n ** 3) + 1j * rng.standard_normal(n ** 3)).cuda()
@@ -61,6 +71,30 @@ def test_sharded_equals_single_gpu_bitwise(b, world):
     plan = so3.make_plan(b)
     ref_f = so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan).data
     ref_i = so3.ifsoft_sequential(so3.So3Coefficients(b, coeffs), plan).data
-    got_f, got_i = emulate(b, world, grid, coeffs)
+    got_f, got_i = emulate(b, world, grid, coeffs, chunks)
     assert torch.equal(got_f, ref_f)
     assert torch.equal(got_i, ref_i)
+
+
+def test_full_dwt_entry_points_walk_all_chunks():
+    """so3_shard_dwt_analysis / _synthesis on a chunked plan equal the per-chunk calls."""
+    b, world, chunks = 32, 2, 3
+    m = ShardMap(b, world, chunks)
+    rng = np.random.default_rng(5)
+    be = NativeShardBackend(b, world, 1, chunks=chunks)
+    C = so3.coeff_count(b)
+    coeffs = torch.from_numpy(rng.standard_normal(C) + 1j * rng.standard_normal(C)).cuda()
+    full = be.empty(m.layout_b_rows(1) * m.J)
+    be.dwt_synthesis(coeffs, full)
+    per = be.empty(m.layout_b_rows(1) * m.J)
+    for q in range(chunks):
+        b0, b1 = m.chunk_b(1, q)
+        be.dwt_synthesis_chunk(q, coeffs, per[b0:b1])
+    assert torch.equal(full, per)
+    c1, c2 = be.zeros(C), be.zeros(C)
+    be.dwt_analysis(full, c1)
+    for q in range(chunks):
+        b0, b1 = m.chunk_b(1, q)
+        be.dwt_analysis_chunk(q, full[b0:b1], c2)
+    assert torch.equal(c1, c2)
+    be.release()
