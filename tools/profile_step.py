@@ -10,6 +10,8 @@ n = 2 * b
 C = b * (4 * b * b - 1) // 3
 F = int(os.environ.get("PROF_BATCH", "1"))
 plan = so3.make_plan(b, batch=F)
+for kv in filter(None, os.environ.get("SO3_KNOBS", "").split(",")):
+    k, v = kv.split("="); plan.set_knob(k, int(v))
 rng = np.random.default_rng(b)
 c = torch.from_numpy(rng.standard_normal(F * C) + 1j * rng.standard_normal(F * C)).cuda()
 grid = torch.empty(F * n ** 3, dtype=torch.complex128, device="cuda")
