@@ -203,7 +203,8 @@ __device__ __forceinline__ void fft_rows(double2 (&v)[16], int t, const double2*
 }
 
 // Stockham path: N in {16..2048} power of two, XB rows per CTA, XB*N/16 threads (tid = xl + XB*t).
-template <int N, int XB, int SIGN, int MINB = (XB * N / 16 <= 256 ? 2 : 1)>
+// TAB: row-table (sharded) addressing compiled in; the plain passes instantiate TAB = false.
+template <int N, int XB, int SIGN, bool TAB = false, int MINB = (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1)>
 __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) {
   extern __shared__ double2 smem[];
   constexpr int TPR = N / 16;  // threads per row
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
   double2* row = smem + xl * RowLayout<N, XB>::SIZE;
 
   double2 v[16];
-  if (a.tab_in) {
+  if (TAB && a.tab_in) {
     const double2* base = a.src + f * a.fs_in + x;
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
@@ -235,6 +236,12 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
       v[e] = zero ? make_double2(0.0, 0.0) : src[(long long)p * a.sp_in];
     }
   }
+  // row-table passes: the output rows are fetched before the transform (off the critical path)
+  int rout[16];
+  if (TAB && a.tab_out) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) rout[e] = __ldg(&a.tab_out[(long long)y * N + t + e * TPR]);
+  }
   fft_rows<N, SIGN>(v, t, a.tw, row);
   double wx = 1.0;
   if (a.weight && xvalid) wx = __ldg(&a.w[a.jbase + x]);
@@ -246,9 +253,8 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
       double2 z = v[e];
       z.x *= wx;
       z.y *= wx;
-      if (a.tab_out) {
-        const int r = __ldg(&a.tab_out[(long long)y * N + p]);
-        if (r >= 0) tbase[(long long)r * a.tabJ] = z;
+      if (TAB && a.tab_out) {
+        if (rout[e] >= 0) tbase[(long long)rout[e] * a.tabJ] = z;
       } else {
         dst[(long long)p * a.sp_out] = z;
       }

@@ -175,7 +175,9 @@ int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st)
   const int threads = XB * N / 16;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
   dim3 grid((a.X + XB - 1) / XB, a.Y, batch);
-  void (*k)(so3::FftArgs) = sign > 0 ? so3::fft_pass_kernel<N, XB, +1> : so3::fft_pass_kernel<N, XB, -1>;
+  const bool tab = a.tab_in || a.tab_out;
+  void (*k)(so3::FftArgs) = sign > 0 ? (tab ? so3::fft_pass_kernel<N, XB, +1, true> : so3::fft_pass_kernel<N, XB, +1, false>)
+                                     : (tab ? so3::fft_pass_kernel<N, XB, -1, true> : so3::fft_pass_kernel<N, XB, -1, false>);
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<grid, threads, smem, st>>>(a);
   SO3_CUDA(cudaGetLastError());
