@@ -262,6 +262,84 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// One-pass 2-D transform of whole beta slices for N = 2B <= 64 (a slice is N*N complex128,
+// 64 KB at N = 64, so it fits in shared memory): the grid side moves through shared memory
+// with coalesced row accesses, the pair-major side is read / written directly (16 bytes per
+// element; CTAs of neighbouring j share every 128-byte line in L2).  Same radix code, in the
+// same order, as the two passes (K1a then K1b, K4a then K4b), so results are bit-identical
+// to them; HBM traffic is one read + one write of the grid instead of two of each.
+//   forward (SIGN +1): grid[f][i][j][k] -> X[f][m'][m][j] * w_j   (m' = nyq not written)
+//   inverse (SIGN -1): X[f][m'][m][j]   -> grid[f][i][j][k]       (m = nyq and m' = nyq read as 0)
+// One CTA per (j, f); thread tid works on row r = tid % N, points t + (N/16) e.
+template <int N, int SIGN>
+__global__ void __launch_bounds__(N * N / 16, (N >= 64 ? 2 : 4)) fft2d_slice_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                                                                  const double2* __restrict__ tw, const double* __restrict__ w,
+                                                                  long long fstride, int nyq) {
+  constexpr int NT = N * N / 16, TPR = N / 16, SIZE = RowLayout<N, N>::SIZE;
+  extern __shared__ double2 E[];   // N rows of SIZE (padded), also the FFT exchange rows
+  const int j = blockIdx.x;
+  const long long f = blockIdx.y;
+  const int tid = threadIdx.x, r = tid % N, t = tid / N;
+  const long long n = N, n2 = n * n;
+  const double2* in = src + f * fstride;
+  double2* out = dst + f * fstride;
+  double2* row = E + r * SIZE;
+  double2 v[16];
+  if (SIGN > 0) {
+    // grid rows (i, j) for all i: coalesced into E[i][pidx(k)]
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + NT * q, i = idx / N, k = idx % N;
+      E[i * SIZE + pidx(k)] = in[((long long)i * n + j) * n + k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * TPR)];
+  } else {
+    // X[m' = r][m][j], m = t + TPR e; the Nyquist row and column are zero
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int m = t + e * TPR;
+      v[e] = (r == nyq || m == nyq) ? make_double2(0.0, 0.0) : in[((long long)r * n + m) * n + j];
+    }
+  }
+  __syncthreads();   // every thread holds its inputs before the rows are reused for exchange
+  fft_rows<N, SIGN>(v, t, tw, row);
+  __syncthreads();
+  // transpose: first-axis outputs become the rows of the second axis
+#pragma unroll
+  for (int e = 0; e < 16; ++e) E[(t + e * TPR) * SIZE + pidx(r)] = v[e];
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * TPR)];
+  __syncthreads();
+  fft_rows<N, SIGN>(v, t, tw, row);
+  if (SIGN > 0) {
+    // v[e] = S(m = t + TPR e, m' = r) -> X[m'][m][j] * w_j
+    if (r != nyq) {
+      const double wj = __ldg(&w[j]);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int m = t + e * TPR;
+        out[((long long)r * n + m) * n + j] = make_double2(v[e].x * wj, v[e].y * wj);
+      }
+    }
+  } else {
+    // v[e] = f(i = r, k = t + TPR e): through E for coalesced grid rows
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) row[pidx(t + e * TPR)] = v[e];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + NT * q, i = idx / N, k = idx % N;
+      out[((long long)i * n + j) * n + k] = E[i * SIZE + pidx(k)];
+    }
+  }
+  (void)n2;
+}
+
 // Direct DFT for non power-of-two or N < 16: a CTA stages XC rows in shared memory and
 // computes every output point of them (O(N^2) per row).
 template <int SIGN>

@@ -163,6 +163,7 @@ struct so3_plan_s {
   int ana_cta = 1;    // analysis: single-CTA 32-degree-tile kernel (SO3_ANA_CTA=0: 2-CTA cluster kernel)
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
+  int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
 };
 
@@ -217,6 +218,29 @@ int launch_fft(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int 
     case 1024: return launch_fft_xb<1024>(a, sign, batch, st, xb_override ? xb_override : 4);
     case 2048: return launch_fft_pow2<2048, 2>(a, sign, batch, st);
     default: return launch_fft_direct(a, sign, batch, st);
+  }
+}
+
+template <int N, int SIGN>
+int launch_fft2d_t(const so3_plan_s* p, const void* src, void* dst, cudaStream_t st) {
+  const size_t smem = (size_t)N * so3::RowLayout<N, N>::SIZE * sizeof(double2);
+  auto k = so3::fft2d_slice_kernel<N, SIGN>;
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(N, p->batch), N * N / 16, smem, st>>>(static_cast<const double2*>(src), static_cast<double2*>(dst), p->d_tw,
+                                               p->d_w, p->ngrid, p->B);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+// One-pass slice transform when a whole beta slice fits in shared memory (2B in {16, 32, 64});
+// returns -1 when it does not apply.
+int launch_fft2d(const so3_plan_s* p, int sign, const void* src, void* dst, cudaStream_t st) {
+  if (!p->fft_fused || p->sharded) return -1;
+  switch (p->n) {
+    case 16: return sign > 0 ? launch_fft2d_t<16, +1>(p, src, dst, st) : launch_fft2d_t<16, -1>(p, src, dst, st);
+    case 32: return sign > 0 ? launch_fft2d_t<32, +1>(p, src, dst, st) : launch_fft2d_t<32, -1>(p, src, dst, st);
+    case 64: return sign > 0 ? launch_fft2d_t<64, +1>(p, src, dst, st) : launch_fft2d_t<64, -1>(p, src, dst, st);
+    default: return -1;
   }
 }
 
@@ -775,6 +799,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
+  if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
@@ -795,6 +820,7 @@ int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* st
   if (samples == spectrum || spectrum == p->d_scratch)
     return fail(SO3_ERR_INVALID, "fft_analysis: spectrum must not alias the samples or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_fft2d(p, +1, samples, spectrum, st); rc >= 0) return rc;
   int rc = launch_fft(fft_pass_args(p, 0, samples, p->d_scratch), +1, p->batch, st, p->fft_wide);
   if (rc) return rc;
   return launch_fft(fft_pass_args(p, 1, p->d_scratch, spectrum), +1, p->batch, st, p->fft_wide);
@@ -805,6 +831,7 @@ int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream)
   if (samples == spectrum || spectrum == p->d_scratch || samples == p->d_scratch)
     return fail(SO3_ERR_INVALID, "fft_synthesis: buffers must not alias each other or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (int rc = launch_fft2d(p, -1, spectrum, samples, st); rc >= 0) return rc;
   int rc = launch_fft(fft_pass_args(p, 2, spectrum, p->d_scratch), -1, p->batch, st, p->fft_wide);
   if (rc) return rc;
   return launch_fft(fft_pass_args(p, 3, p->d_scratch, samples), -1, p->batch, st, p->fft_wide);
