@@ -131,9 +131,11 @@ int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_de
 #define SO3_DWT_MMA 0
 #define SO3_DWT_SIMT 1
 int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
-/* Tuning knobs (same results, different kernel shapes): "dwt_variant", "ana_cta" (analysis
- * kernel: 1 single-CTA 32-degree tiles, 0 two-CTA cluster), "syn_jw" (synthesis beta indices
- * per warp, 0 = default), "fft_xb" (FFT rows per CTA, 0 = default). */
+/* Tuning knobs (same results, different kernel shapes): "dwt_variant" (as above), "syn_jw"
+ * (synthesis beta indices per warp, 0 = default), "fft_xb" (FFT rows per CTA for
+ * 2B in {256, 512, 1024}, 0 = default), "dwt_batch" (1 = dense-contraction DWT for batched
+ * plans with 2B <= 64, 0 = per-function kernels), "fft_fused" (1 = one-pass 2-D slice FFT for
+ * 2B <= 64, 0 = two passes).  Unknown names fail with SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */

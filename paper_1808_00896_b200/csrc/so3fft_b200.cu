@@ -160,7 +160,6 @@ struct so3_plan_s {
   std::vector<int64_t> chunk_pairs;     // this rank's pairs of chunk q
   std::vector<int64_t> chunk_off;       // prefix of chunk_pairs
   int dwt_variant = SO3_DWT_MMA;
-  int ana_cta = 1;    // analysis: single-CTA 32-degree-tile kernel (SO3_ANA_CTA=0: 2-CTA cluster kernel)
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
@@ -336,31 +335,12 @@ int dwt_jw(int n) {
 }
 
 template <int JW, int WPC, int FG = 1>
-int launch_dwt_mma_wpc(bool analysis, const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
+int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
-  if (analysis) {
-    const size_t smem = ((size_t)WPC * SM::DT_ROWS * SM::S + 2 * (size_t)WPC * 256) * sizeof(double);
-    auto k = so3::dwt_analysis_mma_kernel<JW, WPC>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ncl * split, batch);
-    cfg.blockDim = dim3(WPC * 32);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = split;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    SO3_CUDA(cudaLaunchKernelEx(&cfg, k, a));
-  } else {
-    const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
-    auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<dim3(ncl * split, batch / FG), WPC * 32, smem, st>>>(a, split);
-  }
+  const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
+  auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG>;
+  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(ncl * split, batch / FG), WPC * 32, smem, st>>>(a, split);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
@@ -378,18 +358,22 @@ int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cu
 }
 
 template <int JW>
-int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st,
-                   int ana_cta = 0) {
+int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
   const int warps = (n + JW - 1) / JW;
-  if (JW == 32 && batch % 4 == 0 && !analysis) {   // batched small B: 4 functions share each recurrence
-    if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2, 4>(analysis, a, warps / 2, ncl, batch, st);
-    return launch_dwt_mma_wpc<JW, 1, 4>(analysis, a, warps, ncl, batch, st);
+  if (analysis) {
+    if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
+    return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st);
   }
-  if (analysis && ana_cta && warps <= 8) return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st);
-  if (warps > (analysis ? 8 : 16)) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
-  if (warps >= 4 && warps % 4 == 0) return launch_dwt_mma_wpc<JW, 4>(analysis, a, warps / 4, ncl, batch, st);
-  if (warps % 2 == 0) return launch_dwt_mma_wpc<JW, 2>(analysis, a, warps / 2, ncl, batch, st);
-  return launch_dwt_mma_wpc<JW, 1>(analysis, a, warps, ncl, batch, st);
+  if constexpr (JW == 32) {
+    if (batch % 4 == 0) {   // batched small B: 4 functions share each recurrence
+      if (warps % 2 == 0) return launch_dwt_syn_wpc<JW, 2, 4>(a, warps / 2, ncl, batch, st);
+      return launch_dwt_syn_wpc<JW, 1, 4>(a, warps, ncl, batch, st);
+    }
+  }
+  if (warps > 16) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
+  if (warps >= 4 && warps % 4 == 0) return launch_dwt_syn_wpc<JW, 4>(a, warps / 4, ncl, batch, st);
+  if (warps % 2 == 0) return launch_dwt_syn_wpc<JW, 2>(a, warps / 2, ncl, batch, st);
+  return launch_dwt_syn_wpc<JW, 1>(a, warps, ncl, batch, st);
 }
 
 template <int FC, int MTMAX>
@@ -445,9 +429,9 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   }
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
-      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
-      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
-      default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st, p->ana_cta);
+      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
     }
   }
   const int jt = dwt_jt(p->n);
@@ -627,7 +611,6 @@ so3_plan_s* new_plan(int b, int batch) {
   cudaGetDevice(&p->device);
   if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
   if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
-  if (const char* e = getenv("SO3_ANA_CTA")) p->ana_cta = atoi(e);
   if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
   return p;
 }
@@ -795,7 +778,6 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (!p || !name) return fail(SO3_ERR_INVALID, "null plan or knob name");
   const std::string k(name);
   if (k == "dwt_variant") return so3_plan_set_dwt_variant(p, value);
-  if (k == "ana_cta") { p->ana_cta = value; return SO3_OK; }
   if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
