@@ -1,8 +1,9 @@
 """B200-native FSOFT / iFSOFT -- drop-in for the hot path of the reference `so3fft`.
 
 Public names follow the reference's export table (pkg/src/so3fft/__init__.py:17-94)
-for the transform path: containers and layouts (core), grid/weights, clusters,
-make_plan / fsoft_* / ifsoft_*.  Compute runs in libso3fft_b200.so (hand-written
+for the transform path: containers and layouts (core), grid/weights, clusters and the
+sigma / kappa work-index maps, make_plan / fsoft_* / ifsoft_*, the direct route and the
+benchmark harness.  Compute runs in libso3fft_b200.so (hand-written
 sm_100a CUDA, include/so3fft_b200.h); there is no CPU fallback.
 """
 
@@ -47,10 +48,25 @@ from .soft import (
     ifsoft_batch,
     ifsoft_parallel,
     ifsoft_sequential,
+    kappa_count,
+    kappa_split,
+    kappa_to_orders,
     make_plan,
     quadrature_weights,
+    rect_to_orders,
     sample_angles,
+    sigma_index,
+    sigma_inverse,
     wigner_rows,
+)
+from .report import (
+    BenchConfig,
+    BenchRecord,
+    OracleMismatchError,
+    error_metrics,
+    random_coefficients,
+    run_benchmark,
+    write_report,
 )
 
 __version__ = "0.1.0"

@@ -79,24 +79,73 @@ def cluster_for_base(m: int, mp: int) -> SymmetryCluster:
     return SymmetryCluster(kind, OrderPair(m, mp), tuple(members))
 
 
+# ---- the paper's remapping of the order-pair triangle onto flat work indices --------------
+# sigma: row-major triangle 0 <= m' <= m (schedule.py:40-52); kappa: the strict lower triangle
+# 1 <= m' < m <= B-1 folded into a (B-1)/2 x (B-1) rectangle so that an integer divmod
+# splits it (schedule.py:55-90).
+
+def sigma_index(m: int, mp: int) -> int:
+    """Triangle index of a pair with 0 <= m' <= m (reference schedule.py:40-44)."""
+    if not 0 <= mp <= m:
+        raise ValueError(f"require 0 <= m' <= m, got (m={m}, m'={mp})")
+    return m * (m + 1) // 2 + mp
+
+
+def sigma_inverse(sigma: int) -> OrderPair:
+    """Inverse of sigma_index by the same floating-point closed form (schedule.py:47-52)."""
+    if sigma < 0:
+        raise ValueError(f"sigma must be >= 0, got {sigma}")
+    m = int(math.floor(math.sqrt(2.0 * sigma + 0.25) - 0.5))
+    return OrderPair(m, sigma - m * (m + 1) // 2)
+
+
+def rect_to_orders(i: int, j: int, bandwidth: int) -> OrderPair:
+    """Rectangle cell (i, j), 1 <= i <= (B-1)//2, 1 <= j <= B-1 -> strict-lower-triangle
+    pair (schedule.py:59-70).  Cells right of the diagonal fold onto the far corner."""
+    b = validate_bandwidth(bandwidth)
+    rows = (b - 1) // 2
+    if not 1 <= i <= rows:
+        raise ValueError(f"row i={i} outside [1, {rows}] for B={b}")
+    if not 1 <= j <= b - 1:
+        raise ValueError(f"column j={j} outside [1, {b - 1}] for B={b}")
+    if b % 2 == 1 and i == rows and j > rows:
+        raise ValueError(f"cell (i={i}, j={j}) beyond the half row of odd B={b}")
+    return OrderPair(b - i, b - j) if j > i else OrderPair(i + 1, j)
+
+
+def kappa_count(bandwidth: int) -> int:
+    """(B-1)(B-2)/2 strict-lower-triangle pairs (schedule.py:73-76)."""
+    b = validate_bandwidth(bandwidth)
+    return (b - 1) * (b - 2) // 2
+
+
+def kappa_split(kappa: int, bandwidth: int) -> tuple[int, int]:
+    """Integer split of a work index into its rectangle cell (schedule.py:79-84)."""
+    b = validate_bandwidth(bandwidth)
+    if not 0 <= kappa < kappa_count(b):
+        raise ValueError(f"kappa={kappa} outside [0, {kappa_count(b)}) for B={b}")
+    return kappa // (b - 1) + 1, kappa % (b - 1) + 1
+
+
+def kappa_to_orders(kappa: int, bandwidth: int) -> OrderPair:
+    """Base order pair of work index kappa (schedule.py:87-90)."""
+    i, j = kappa_split(kappa, bandwidth)
+    return rect_to_orders(i, j, bandwidth)
+
+
 def enumerate_clusters(bandwidth: int, partitioner: str = "kappa") -> list[SymmetryCluster]:
     """All symmetry clusters below B in the reference's order (schedule.py:136-158).
 
-    "kappa": origin, axis, diagonal, then the kappa rectangle (integer divmod split,
-    schedule.py:59-90); "sigma": triangle order (schedule.py:40-52).  The GPU launch
-    order is cluster_schedule(); both cover the (2B-1)^2 order pairs exactly once.
+    "kappa": origin, axis, diagonal, then the kappa rectangle; "sigma": triangle order.
+    The GPU launch order is cluster_schedule(); both cover the (2B-1)^2 order pairs
+    exactly once.
     """
     b = validate_bandwidth(bandwidth)
     if partitioner == "kappa":
         bases = [(0, 0)] + [(m, 0) for m in range(1, b)] + [(m, m) for m in range(1, b)]
-        for kappa in range((b - 1) * (b - 2) // 2):
-            i, j = kappa // (b - 1) + 1, kappa % (b - 1) + 1
-            bases.append((b - i, b - j) if j > i else (i + 1, j))
+        bases += [tuple(kappa_to_orders(k, b)) for k in range(kappa_count(b))]
     elif partitioner == "sigma":
-        bases = []
-        for s in range(b * (b + 1) // 2):
-            m = int(math.floor(math.sqrt(2.0 * s + 0.25) - 0.5))
-            bases.append((m, s - m * (m + 1) // 2))
+        bases = [tuple(sigma_inverse(s)) for s in range(b * (b + 1) // 2)]
     else:
         raise ValueError(f"unknown partitioner {partitioner!r}")
     return [cluster_for_base(m, mp) for m, mp in bases]

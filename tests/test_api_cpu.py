@@ -95,3 +95,32 @@ def test_binary_header_and_rejections(tmp_path):
     bad.data[3] = np.nan
     with pytest.raises(ValueError):
         so3.write_coefficients(str(tmp_path / "nan.sofc"), bad)
+
+
+def test_work_index_maps_follow_the_reference(golden):
+    """sigma / kappa maps (reference schedule.py:40-90): the kappa part of the golden
+    cluster order (after origin, axes, diagonals) is kappa_to_orders(0..), and both maps
+    cover their triangles exactly once."""
+    g = golden("schedule.npz")
+    for b in (3, 4, 7, 8, 16, 33):
+        kap = [tuple(x) for x in g[f"bases_b{b}"]][1 + 2 * (b - 1):]
+        assert [tuple(so3.kappa_to_orders(k, b)) for k in range(so3.kappa_count(b))] == kap
+        assert {tuple(so3.kappa_to_orders(k, b)) for k in range(so3.kappa_count(b))} == \
+            {(m, mp) for m in range(2, b) for mp in range(1, m)}
+    for s in range(500):
+        m, mp = so3.sigma_inverse(s)
+        assert so3.sigma_index(m, mp) == s and 0 <= mp <= m
+    assert so3.kappa_split(0, 8) == (1, 1) and so3.kappa_split(so3.kappa_count(8) - 1, 8) == (3, 7)
+    assert so3.kappa_count(1) == 0 and so3.kappa_count(2) == 0
+
+
+@pytest.mark.parametrize("call", [
+    lambda: so3.sigma_index(2, 3), lambda: so3.sigma_index(3, -1), lambda: so3.sigma_inverse(-1),
+    lambda: so3.kappa_split(so3.kappa_count(6), 6), lambda: so3.kappa_split(-1, 6),
+    lambda: so3.rect_to_orders(0, 1, 8), lambda: so3.rect_to_orders(4, 1, 8), lambda: so3.rect_to_orders(1, 8, 8),
+    lambda: so3.rect_to_orders(3, 4, 7),   # beyond the half row of odd B
+    lambda: so3.kappa_count(0),
+])
+def test_work_index_maps_reject_like_the_reference(call):
+    with pytest.raises(ValueError):
+        call()
