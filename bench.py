@@ -512,6 +512,43 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     ms_step = ms_total / args.steps
     # parity: gathered coefficients of the measured step == seeded input (round trip)
     full = sh.gather_coefficients(result["coeffs"].clone())
+
+    # e2e through the sharded public API: every step moves this rank's inputs in from pinned
+    # host memory (coefficients, then its beta slab) and its outputs back (slab, coefficients)
+    e2e = None
+    if not args.no_e2e:
+        h_c = torch.empty(C, dtype=torch.complex128, pin_memory=True)
+        h_c.copy_(torch.from_numpy(host_c))
+        h_slab = torch.empty(n * J * n, dtype=torch.complex128, pin_memory=True)
+        h_out = torch.empty(C, dtype=torch.complex128, pin_memory=True)
+
+        def e2e_step():
+            c_dev = h_c.to(dev, non_blocking=True)
+            h_slab.copy_(sh.ifsoft(c_dev), non_blocking=True)
+            s_dev = h_slab.to(dev, non_blocking=True)
+            h_out.copy_(sh.fsoft(s_dev), non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if dist is not None:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1) / args.e2e_steps
+        if dist is not None:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        io = 16 * (C + n * J * n)
+        e2e = {"value": 2.0 * 1000.0 / e_ms, "unit": "transforms/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": io, "d2h_bytes_per_step": io, "steps": args.e2e_steps,
+               "api": "ShardedSO3.ifsoft(coefficients H2D) -> slab D2H; slab H2D -> ShardedSO3.fsoft -> own "
+                      "coefficient slots D2H (per rank, pinned host buffers)"}
     got = full.cpu().numpy()
     diff = np.abs(got - host_c)
     if rank != 0:
@@ -546,7 +583,7 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
         "stages_rank0_ms": stage_ms,
         "roofline": roof,
         "all_to_all": a2a,
-        "cpu_baseline": None, "e2e": None, "gpu_launches": (4 + 2 * chunks) * args.steps,
+        "cpu_baseline": None, "e2e": e2e, "gpu_launches": (4 + 2 * chunks) * args.steps,
         "clocks": clk,
         "parity": {"roundtrip_max_abs": float(diff.max()),
                    "roundtrip_max_rel_of_max": float(diff.max() / np.abs(host_c).max())},
