@@ -327,6 +327,30 @@ def _stream(plan: TransformPlan):
     return ctypes.c_void_p(torch.cuda.current_stream(plan.device).cuda_stream)
 
 
+def _device_buffer(t, count: int, plan: TransformPlan, what: str):
+    """A caller-supplied device buffer the kernels read or write ``count`` complex128 (or, for
+    float buffers, float64) elements of: checked before its pointer crosses the C ABI."""
+    torch = _torch()
+    if not _is_torch(t) or not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if t.device != plan.device:
+        raise ValueError(f"{what} on {t.device}, plan on {plan.device}")
+    if t.dtype != torch.complex128:
+        raise ValueError(f"{what} must be complex128, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    if t.numel() != count:
+        raise ValueError(f"{what} must hold {count} elements, got {t.numel()}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _disjoint(a, a_bytes: int, b, b_bytes: int, what: str) -> None:
+    pa = a.data_ptr() if _is_torch(a) else a.ctypes.data
+    pb = b.data_ptr() if _is_torch(b) else b.ctypes.data
+    if pa < pb + b_bytes and pb < pa + a_bytes:
+        raise ValueError(f"{what}: output must not overlap the input")
+
+
 def _run(plan: TransformPlan, data, out_count: int, dev_fn: str, host_fn: str, out=None):
     """Dispatch a whole transform on device tensors or host arrays (batch-aware)."""
     torch = _torch()
@@ -342,6 +366,9 @@ def _run(plan: TransformPlan, data, out_count: int, dev_fn: str, host_fn: str, o
             raise ValueError("device data must be complex128")
         if out is None:
             out = torch.empty(total, dtype=torch.complex128, device=plan.device)
+        else:
+            _device_buffer(out, total, plan, "out")
+            _disjoint(out, 16 * total, data, 16 * data.numel(), dev_fn)
         with torch.cuda.device(plan.device):
             _native.check(getattr(lib, dev_fn)(plan.handle, ctypes.c_void_p(data.data_ptr()),
                                                ctypes.c_void_p(out.data_ptr()), _stream(plan)), dev_fn)
@@ -349,6 +376,11 @@ def _run(plan: TransformPlan, data, out_count: int, dev_fn: str, host_fn: str, o
     arr = np.ascontiguousarray(data, dtype=np.complex128)
     if out is None:
         out = np.empty(total, dtype=np.complex128)
+    else:
+        if not isinstance(out, np.ndarray) or out.dtype != np.complex128 or not out.flags.c_contiguous \
+                or not out.flags.writeable or out.size != total:
+            raise ValueError(f"out must be a writeable C-contiguous complex128 numpy array of {total} elements")
+        _disjoint(out, 16 * total, arr, 16 * arr.size, host_fn)
     with torch.cuda.device(plan.device):
         _native.check(getattr(lib, host_fn)(plan.handle, ctypes.c_void_p(arr.ctypes.data),
                                             ctypes.c_void_p(out.ctypes.data), _stream(plan)), host_fn)
@@ -426,30 +458,42 @@ def _ptr(t) -> ctypes.c_void_p:
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _grid_count(plan: TransformPlan) -> int:
+    return plan.batch * grid_size(plan.bandwidth) ** 3
+
+
+def _coef_count(plan: TransformPlan) -> int:
+    return plan.batch * coeff_count(plan.bandwidth)
+
+
 def fft_analysis(plan: TransformPlan, samples, spectrum) -> None:
     """K1: weighted torus spectrum spectrum[f][m'][m][j] of device samples (fft.py:72-76, soft.py:130-132)."""
-    _native.check(_native.lib().so3_fft_analysis(plan.handle, _ptr(samples), _ptr(spectrum), _stream(plan)),
-                  "fft_analysis")
+    ps = _device_buffer(samples, _grid_count(plan), plan, "samples")
+    pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
+    _native.check(_native.lib().so3_fft_analysis(plan.handle, ps, pz, _stream(plan)), "fft_analysis")
 
 
 def fft_synthesis(plan: TransformPlan, spectrum, samples) -> None:
     """K4: samples from spectrum[f][m'][m][j] (soft.py:164-172); spectrum is read only."""
-    _native.check(_native.lib().so3_fft_synthesis(plan.handle, _ptr(spectrum), _ptr(samples), _stream(plan)),
-                  "fft_synthesis")
+    pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
+    ps = _device_buffer(samples, _grid_count(plan), plan, "samples")
+    _native.check(_native.lib().so3_fft_synthesis(plan.handle, pz, ps, _stream(plan)), "fft_synthesis")
 
 
 def dwt_analysis(plan: TransformPlan, spectrum, coeffs, begin: int = 0, end: int | None = None) -> None:
     """K2: forward DWT of clusters [begin, end) of the launch schedule (dwt.py:109-116)."""
     end = plan.n_clusters if end is None else end
-    _native.check(_native.lib().so3_dwt_analysis(plan.handle, _ptr(spectrum), _ptr(coeffs), begin, end,
-                                                  _stream(plan)), "dwt_analysis")
+    pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
+    pc = _device_buffer(coeffs, _coef_count(plan), plan, "coeffs")
+    _native.check(_native.lib().so3_dwt_analysis(plan.handle, pz, pc, begin, end, _stream(plan)), "dwt_analysis")
 
 
 def dwt_synthesis(plan: TransformPlan, coeffs, spectrum, begin: int = 0, end: int | None = None) -> None:
     """K3: inverse DWT of clusters [begin, end) (dwt.py:119-125)."""
     end = plan.n_clusters if end is None else end
-    _native.check(_native.lib().so3_dwt_synthesis(plan.handle, _ptr(coeffs), _ptr(spectrum), begin, end,
-                                                   _stream(plan)), "dwt_synthesis")
+    pc = _device_buffer(coeffs, _coef_count(plan), plan, "coeffs")
+    pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
+    _native.check(_native.lib().so3_dwt_synthesis(plan.handle, pc, pz, begin, end, _stream(plan)), "dwt_synthesis")
 
 
 def wigner_rows(plan: TransformPlan, m: int, mp: int):

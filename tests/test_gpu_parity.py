@@ -437,3 +437,32 @@ def test_report_harness_on_gpu(tmp_path):
     assert (tmp_path / "g.sofg").exists() and (tmp_path / "c.sofc").exists()
     assert R.main(["--bandwidths", "4", "--threads", "1", "--runs", "1", "--oracle",
                    "--output", str(tmp_path / "r.csv")]) == 0
+
+
+def test_caller_buffers_are_validated_before_any_kernel():
+    """Outputs and stage buffers cross the C ABI as raw pointers: wrong length, dtype, device,
+    layout or an output overlapping the input must raise instead of being overrun."""
+    b = 4
+    n, C = 2 * b, O.n_coeffs(b)
+    plan = plan_for(b)
+    grid = torch.zeros(n ** 3, dtype=torch.complex128, device="cuda")
+    coef = torch.zeros(C, dtype=torch.complex128, device="cuda")
+    bad_outs = [torch.zeros(C - 1, dtype=torch.complex128, device="cuda"),
+                torch.zeros(C, dtype=torch.complex64, device="cuda"),
+                torch.zeros(2 * C, dtype=torch.complex128, device="cuda")[::2],
+                torch.zeros(C, dtype=torch.complex128)]
+    for out in bad_outs:
+        with pytest.raises(ValueError):
+            so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan, out=out)
+    with pytest.raises(ValueError):
+        so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan, out=grid[:C])      # overlaps the input
+    with pytest.raises(ValueError):
+        so3.ifsoft_sequential(so3.So3Coefficients(b, coef.cpu().numpy()), plan, out=np.zeros(n ** 3 - 1, np.complex128))
+    with pytest.raises(ValueError):
+        so3.fft_analysis(plan, grid, torch.zeros(n ** 3 - 8, dtype=torch.complex128, device="cuda"))
+    with pytest.raises(ValueError):
+        so3.dwt_analysis(plan, grid.cpu(), coef)
+    with pytest.raises(ValueError):
+        so3.dwt_synthesis(plan, coef[:-1], grid)
+    ok = torch.empty(C, dtype=torch.complex128, device="cuda")
+    assert so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan, out=ok).data.data_ptr() == ok.data_ptr()
