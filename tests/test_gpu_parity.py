@@ -466,3 +466,24 @@ def test_caller_buffers_are_validated_before_any_kernel():
         so3.dwt_synthesis(plan, coef[:-1], grid)
     ok = torch.empty(C, dtype=torch.complex128, device="cuda")
     assert so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan, out=ok).data.data_ptr() == ok.data_ptr()
+
+
+def test_wigner_recurrence_at_b512_against_50_digit_values(golden):
+    """The rescaled fp64 recurrence on the GPU against d^l_{m,m'}(beta_j) evaluated with
+    mpmath at 50 digits (oracle/gen_wigner_mp.py) for degrees up to 511 and members of every
+    relation.  The bound is the reference's own fp64 recurrence error on the same entries."""
+    g = golden("wigner_mp_b512.npz")
+    plan = plan_for(512)
+    got = np.empty_like(g["value"])
+    pairs = {}
+    for i, (m, mp) in enumerate(zip(g["m"].tolist(), g["mp"].tolist())):
+        pairs.setdefault((m, mp), []).append(i)
+    for (m, mp), idx in pairs.items():
+        rows = so3.wigner_rows(plan, m, mp).cpu().numpy()
+        lo = max(abs(m), abs(mp))
+        for i in idx:
+            got[i] = rows[g["l"][i] - lo, g["j"][i]]
+    err = np.abs(got - g["value"])
+    ref_err = np.abs(g["ref_fp64"] - g["value"])
+    assert err.max() <= max(ref_err.max(), 1e-13), (err.max(), ref_err.max())
+    assert err.max() < 5e-12
