@@ -376,19 +376,19 @@ int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, in
   return launch_dwt_syn_wpc<JW, 1>(a, warps, ncl, batch, st);
 }
 
-template <int FC, int MTMAX>
+// Batched plans with 2B <= 64: analysis 4 functions per CTA (register operands), synthesis
+// 8 functions per CTA (staged coefficients), see dwt_batch.cuh.
 int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
-  const dim3 grid(ncl, (batch + FC - 1) / FC);
   if (analysis) {
-    const size_t smem = so3::batch_analysis_smem<FC>(n);
-    auto k = so3::dwt_analysis_batch_kernel<FC, MTMAX / 4>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, FC * 32, smem, st>>>(a, batch);
+    constexpr int FC = 4;
+    auto k = so3::dwt_analysis_batch_reg_kernel<FC, 16>;
+    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, so3::batch_analysis_smem(n), st>>>(a, batch);
   } else {
+    constexpr int FC = 8;
     const size_t smem = so3::batch_synthesis_smem<FC>(n);
-    auto k = so3::dwt_synthesis_batch_kernel<FC, MTMAX>;
+    auto k = so3::dwt_synthesis_batch_kernel<FC, 8>;
     SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k<<<grid, FC * 32, smem, st>>>(a, batch);
+    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, smem, st>>>(a, batch);
   }
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -421,7 +421,7 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.slab_stride = p->sharded ? (long long)(chunk_pairs >= 0 ? chunk_pairs : p->pairs_rank) * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
-    return launch_dwt_batch<8, 8>(ANALYSIS, a, p->n, ncl, p->batch, st);
+    return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
   const int syn_jw = p->syn_jw ? p->syn_jw : (p->n == 512 ? 64 : 0);
   if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && syn_jw && (p->n + syn_jw - 1) / syn_jw <= 16) {
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
