@@ -153,7 +153,7 @@ struct so3_plan_s {
   int sharded = 0, world = 1, rank = 0, J = 0, jbase = 0;
   int64_t pairs_rank = 0;               // order pairs owned by this rank (DWT rows)
   std::vector<int64_t> pairs_of;        // pairs per rank
-  int* d_row_global = nullptr;          // (m' bin)*n + (m bin) -> row of layout [rank g][pairs_g][J], -1 if none
+  int* d_row_global = nullptr;          // (m' bin)*n + (m bin) -> row of layout A [chunk q][rank g][pairs_{g,q}], -1 if none
   int* d_row_local = nullptr;           // same index -> row among this rank's pairs of its chunk, -1 if not owned
   int chunks = 1;                       // exchange chunks (layouts are chunk-major, see the header)
   std::vector<int64_t> chunk_cl;        // this rank's clusters of chunk q: [chunk_cl[q], chunk_cl[q+1])
