@@ -158,6 +158,48 @@ __device__ __forceinline__ void stockham_stage(double2 (&v)[16], int t, const do
   }
 }
 
+// Last stage (span NS = N / R, Q = 16 / R butterflies per thread at b = t + q N/16): its
+// twiddle w^(r b) = w^(r t) * exp(SIGN 2 pi i r q / 16), so only tb[r] = w^(r t), r < R, come
+// from the table -- loaded by the caller before the preceding exchange -- and the q factor is a
+// compile-time 16th root (ncu: the last stage of N = 1024 stalled 60 % on its 12 table loads;
+// B = 512 FFT stages 16.3 / 15.0 -> 15.2 / 14.7 ms).  Used for R >= 4; with R = 2 the extra
+// constant multiplies cost more than the loads they save.
+template <int N, int SIGN, int R>
+__device__ __forceinline__ void last_twiddles(double2 (&tb)[R], int t, const double2* __restrict__ tw) {
+#pragma unroll
+  for (int r = 1; r < R; ++r) {
+    double2 w = tw[r * t];
+    if constexpr (SIGN < 0) w.y = -w.y;
+    tb[r] = w;
+  }
+}
+
+// u[r] *= tb[r] * exp(SIGN 2 pi i r QI / 16), r = RI..R-1 (QI = 0: the plain table twiddle)
+template <int R, int SIGN, int QI, int RI>
+__device__ __forceinline__ void twiddle_q(double2 (&u)[R], const double2 (&tb)[R]) {
+  if constexpr (RI < R) {
+    u[RI] = wmul16<(RI * QI) & 15, SIGN>(cmul(u[RI], tb[RI]));
+    twiddle_q<R, SIGN, QI, RI + 1>(u, tb);
+  }
+}
+
+template <int N, int R, int SIGN, int Q, int QI>
+__device__ __forceinline__ void last_stage_q(double2 (&v)[16], const double2 (&tb)[R]) {
+  double2 u[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) u[r] = v[QI + r * Q];
+  twiddle_q<R, SIGN, QI, 1>(u, tb);
+  dft_reg<R, SIGN>(u);
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[QI + r * Q] = u[r];
+  if constexpr (QI + 1 < Q) last_stage_q<N, R, SIGN, Q, QI + 1>(v, tb);
+}
+
+template <int N, int R, int SIGN>
+__device__ __forceinline__ void last_stage(double2 (&v)[16], const double2 (&tb)[R]) {
+  last_stage_q<N, R, SIGN, 16 / R, 0>(v, tb);
+}
+
 template <int N>
 struct Radix {
   // N = 16^a * rem; stages: a radix-16 stages then one radix-rem stage (rem in {2,4,8}) if rem > 1.
@@ -171,34 +213,50 @@ template <int N, int SIGN>
 __device__ __forceinline__ void fft_rows(double2 (&v)[16], int t, const double2* __restrict__ tw,
                                          double2* __restrict__ row) {
   using RX = Radix<N>;
-  // stage 1: radix 16, NS = 1
-  if constexpr (RX::N16 == 1 && RX::REM == 1) {
-    stockham_stage<N, 16, 1, SIGN, true>(v, t, tw, row);
-  } else {
-    stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
+  // exchange: every thread's 16 points of the next stage, N/16 apart
+  auto exchange = [&]() {
     __syncthreads();
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
     __syncthreads();
-    if constexpr (RX::N16 == 1) {
+  };
+  // stage 1: radix 16, NS = 1
+  if constexpr (RX::N16 == 1 && RX::REM == 1) {
+    stockham_stage<N, 16, 1, SIGN, true>(v, t, tw, row);
+  } else if constexpr (RX::N16 == 1) {             // N = 32, 64, 128: last stage radix REM, NS = 16
+    stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
+    if constexpr (RX::REM >= 4) {
+      double2 tb[RX::REM];
+      last_twiddles<N, SIGN, RX::REM>(tb, t, tw);  // in flight across the exchange
+      exchange();
+      last_stage<N, RX::REM, SIGN>(v, tb);
+    } else {
+      exchange();
       stockham_stage<N, RX::REM, 16, SIGN, true>(v, t, tw, row);
-    } else if constexpr (RX::N16 == 2 && RX::REM == 1) {
-      stockham_stage<N, 16, 16, SIGN, true>(v, t, tw, row);
-    } else if constexpr (RX::N16 == 2) {
-      stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
-      __syncthreads();
-      stockham_stage<N, RX::REM, 256, SIGN, true>(v, t, tw, row);
-    } else {  // N16 == 3 (N = 4096)
-      stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
-      __syncthreads();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
-      __syncthreads();
-      stockham_stage<N, 16, 256, SIGN, true>(v, t, tw, row);
     }
+  } else if constexpr (RX::N16 == 2 && RX::REM == 1) {   // N = 256
+    stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
+    exchange();
+    stockham_stage<N, 16, 16, SIGN, true>(v, t, tw, row);
+  } else if constexpr (RX::N16 == 2) {             // N = 512, 1024, 2048: last stage radix REM, NS = 256
+    stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
+    exchange();
+    stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
+    if constexpr (RX::REM >= 4) {
+      double2 tb[RX::REM];
+      last_twiddles<N, SIGN, RX::REM>(tb, t, tw);  // in flight across the exchange
+      exchange();
+      last_stage<N, RX::REM, SIGN>(v, tb);
+    } else {
+      exchange();
+      stockham_stage<N, RX::REM, 256, SIGN, true>(v, t, tw, row);
+    }
+  } else {                                         // N16 == 3 (N = 4096)
+    stockham_stage<N, 16, 1, SIGN, false>(v, t, tw, row);
+    exchange();
+    stockham_stage<N, 16, 16, SIGN, false>(v, t, tw, row);
+    exchange();
+    stockham_stage<N, 16, 256, SIGN, true>(v, t, tw, row);
   }
 }
 
