@@ -502,7 +502,7 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
         rec(0)
         sl = sh.ifsoft(coeffs)
         rec(1)
-        result["coeffs"] = sh.fsoft(sl)
+        result["coeffs"] = sh.fsoft(sl, out=out)   # own slots rewritten every step; the rest stay zero
         rec(2)
 
     step = step_staged if chunks == 1 else step_pipelined

@@ -212,8 +212,10 @@ class ShardedSO3:
                                       input_split_sizes=[2 * s for s in send_splits], group=self.group,
                                       async_op=async_op)
 
-    def fsoft(self, slab):
-        """This rank's beta slab [i][jj][k] -> coefficients (own slots; others zero).
+    def fsoft(self, slab, out=None):
+        """This rank's beta slab [i][jj][k] -> coefficients: this rank's slots are written, the
+        others are zero (a fresh array) or left as they are in ``out`` (reuse a buffer zeroed
+        once to skip a full-length memset per call).
         All chunk exchanges are queued behind the FFT; the DWT of chunk q waits for chunk q
         only (on the device stream for NCCL), so it overlaps the exchange of chunks > q."""
         m, r = self.map, self.rank
@@ -226,7 +228,7 @@ class ShardedSO3:
             b0, b1 = m.chunk_b(r, q)
             works.append(self._all_to_all(recv[b0:b1], send[a0:a1], m.forward_recv_splits(r, q),
                                           m.forward_send_splits(r, q), async_op=True))
-        coeffs = self.backend.zeros(self.coeff_count)
+        coeffs = self.backend.zeros(self.coeff_count) if out is None else out
         for q in range(self.chunks):
             if works[q] is not None:
                 works[q].wait()
