@@ -469,12 +469,14 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     stream = torch.cuda.current_stream(dev)
     host_c = seeded_coefficients(b, b)
     coeffs = torch.from_numpy(host_c).to(dev)
-    # buffers reused across steps (the exchange is the only collective)
-    send_b = backend.empty(m.layout_b_rows(rank) * J)
-    recv_a = backend.empty(m.layout_a_rows() * J)
-    send_a = backend.empty(m.layout_a_rows() * J)
-    recv_b = backend.empty(m.layout_b_rows(rank) * J)
-    slab = backend.empty(n * J * n)
+    # staged step (one chunk): buffers reused across steps (the exchange is the only collective);
+    # the pipelined step allocates through ShardedSO3 (torch's caching allocator reuses them)
+    if chunks == 1:
+        send_b = backend.empty(m.layout_b_rows(rank) * J)
+        recv_a = backend.empty(m.layout_a_rows() * J)
+        send_a = backend.empty(m.layout_a_rows() * J)
+        recv_b = backend.empty(m.layout_b_rows(rank) * J)
+        slab = backend.empty(n * J * n)
     out = backend.zeros(C)
 
     result = {}
@@ -645,13 +647,14 @@ def main() -> None:
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
-    if world > 1:
+    mode = args.mode if args.mode != "auto" else ("single" if world == 1 else "sharded")
+    # under torchrun the sharded arm always goes through NCCL, also with one rank (self exchange)
+    if world > 1 or (mode == "sharded" and "MASTER_ADDR" in os.environ):
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         tdist.init_process_group("nccl")
         dist = tdist
-    mode = args.mode if args.mode != "auto" else ("single" if world == 1 else "sharded")
     if mode == "sharded":
         run_sharded_arm(args, rank, world, dist)
     else:

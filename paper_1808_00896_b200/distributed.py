@@ -204,7 +204,7 @@ class ShardedSO3:
 
     def _all_to_all(self, recv, send, recv_splits, send_splits, async_op=False):
         import torch.distributed as dist
-        if self.world == 1:
+        if self.world == 1 and not (dist.is_available() and dist.is_initialized()):
             recv.copy_(send)
             return None
         return dist.all_to_all_single(_as_real(recv), _as_real(send),

@@ -98,3 +98,24 @@ def test_full_dwt_entry_points_walk_all_chunks():
         be.dwt_analysis_chunk(q, full[b0:b1], c2)
     assert torch.equal(c1, c2)
     be.release()
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_sharded_bench_under_torchrun_nccl(chunks):
+    """The multi-GPU bench arm end to end under torchrun with one rank: NCCL process group,
+    all_to_all_single per chunk (self exchange), e2e, max-over-ranks timing; the gathered
+    round trip must recover the seeded coefficients."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(29500 + chunks), "bench.py", "--gpus", "1",
+           "--mode", "sharded", "-B", "64", "--steps", "2", "--warmup", "3", "--chunks", str(chunks),
+           "--e2e-steps", "1", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 1 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["parity"]["roundtrip_max_rel_of_max"] < 1e-12
