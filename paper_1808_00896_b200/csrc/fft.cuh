@@ -209,16 +209,22 @@ struct Radix {
   static constexpr int REM = 1 << (LOG % 4);
 };
 
-template <int N, int SIGN>
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// The exchanges synchronise the threads sharing `row` through `sync` (the whole CTA, or one
+// named-barrier group of a multi-team CTA).
+template <int N, int SIGN, class Sync = CtaSync>
 __device__ __forceinline__ void fft_rows(double2 (&v)[16], int t, const double2* __restrict__ tw,
-                                         double2* __restrict__ row) {
+                                         double2* __restrict__ row, Sync sync = Sync()) {
   using RX = Radix<N>;
   // exchange: every thread's 16 points of the next stage, N/16 apart
   auto exchange = [&]() {
-    __syncthreads();
+    sync();
 #pragma unroll
     for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * (N / 16))];
-    __syncthreads();
+    sync();
   };
   // stage 1: radix 16, NS = 1
   if constexpr (RX::N16 == 1 && RX::REM == 1) {

@@ -22,6 +22,7 @@
 #include "dwt_mma.cuh"
 #include "dwt_batch.cuh"
 #include "fft.cuh"
+#include "fft_tma.cuh"
 #include "direct.cuh"
 
 namespace {
@@ -163,6 +164,7 @@ struct so3_plan_s {
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
+  int fft_tma = 1;    // 2B = 1024: TMA-fed chunks-in passes (fft_tma.cuh); 2: also 2B = 256, 512
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
 };
 
@@ -194,6 +196,64 @@ int launch_fft_direct(const so3::FftArgs& a, int sign, int batch, cudaStream_t s
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+// TMA-fed pass (fft_tma.cuh): RI passes read rows / write chunks, CI passes the reverse.  The
+// chunk side is described by a 5-D tensor map over (x as doubles, p mod 256, p / 256, y, f).
+// TMA-fed chunks-in pass (fft_tma.cuh, K4a / K4b).  The chunk side is described by a 5-D
+// tensor map over (x as doubles, p mod 256, p / 256, y, f), box (8, p_lo, p_hi, 1, 1).
+template <int N, int SIGN>
+int launch_fft_tma_t(const so3::FftArgs& a, int batch, int device, cudaStream_t st) {
+  using TG = so3::TmaGeom<N>;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return fail(SO3_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+  const int plo = N < 256 ? N : 256, phi = N / plo;
+  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_in * 16, (cuuint64_t)plo * a.sp_in * 16, (cuuint64_t)a.sy_in * 16,
+                                 (cuuint64_t)std::max<long long>(a.fs_in, 1) * 16};
+  const cuuint32_t box[5] = {(cuuint32_t)(2 * TG::XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMap map;
+  const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(a.src), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(SO3_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  so3::FftTmaArgs t;
+  t.X = a.X; t.Y = a.Y; t.skip_y = a.skip_y; t.zero_p = a.zero_p;
+  t.ntiles = (long long)(a.X / TG::XB) * (a.Y - (a.skip_y >= 0 ? 1 : 0)) * batch;
+  t.rows_dst = a.dst;
+  t.fs = a.fs_out; t.sy = a.sy_out; t.sx = a.sx_out;
+  t.tw = a.tw;
+  auto k = so3::fft_tma_kernel<N, SIGN>;
+  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
+  int sms = 0;
+  SO3_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const long long grid = std::min<long long>(sms, t.ntiles);
+  if (grid < 1) return SO3_OK;
+  k<<<(unsigned)grid, TG::G * TG::TPG, TG::SMEM, st>>>(map, t);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+// returns -1 when the TMA pass does not apply (row tables, odd sizes, knob off)
+int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st);
 
 // XB (rows per CTA) = the chunk width on the transposed side (XB * 16 bytes).
 template <int N>
@@ -239,6 +299,20 @@ int launch_fft2d(const so3_plan_s* p, int sign, const void* src, void* dst, cuda
     case 16: return sign > 0 ? launch_fft2d_t<16, +1>(p, src, dst, st) : launch_fft2d_t<16, -1>(p, src, dst, st);
     case 32: return sign > 0 ? launch_fft2d_t<32, +1>(p, src, dst, st) : launch_fft2d_t<32, -1>(p, src, dst, st);
     case 64: return sign > 0 ? launch_fft2d_t<64, +1>(p, src, dst, st) : launch_fft2d_t<64, -1>(p, src, dst, st);
+    default: return -1;
+  }
+}
+
+int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st) {
+  // chunks-in passes only (K4a, K4b); measured faster than fft_pass_kernel at 2B = 1024 only
+  // (fft_tma = 2 enables 2B = 256 and 512 as well, for measurements)
+  if (!p->fft_tma || p->fft_wide || a.tab_in || a.tab_out || a.X % 4 || a.weight) return -1;
+  if (a.sp_in == 1 || a.sx_in != 1 || a.sp_out != 1) return -1;
+  if (a.n != 1024 && p->fft_tma < 2) return -1;
+  switch (a.n) {
+    case 256: return sign > 0 ? launch_fft_tma_t<256, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<256, -1>(a, p->batch, p->device, st);
+    case 512: return sign > 0 ? launch_fft_tma_t<512, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<512, -1>(a, p->batch, p->device, st);
+    case 1024: return sign > 0 ? launch_fft_tma_t<1024, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<1024, -1>(a, p->batch, p->device, st);
     default: return -1;
   }
 }
@@ -782,6 +856,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
+  if (k == "fft_tma") { p->fft_tma = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
@@ -803,9 +878,11 @@ int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* st
     return fail(SO3_ERR_INVALID, "fft_analysis: spectrum must not alias the samples or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = launch_fft2d(p, +1, samples, spectrum, st); rc >= 0) return rc;
-  int rc = launch_fft(fft_pass_args(p, 0, samples, p->d_scratch), +1, p->batch, st, p->fft_wide);
-  if (rc) return rc;
-  return launch_fft(fft_pass_args(p, 1, p->d_scratch, spectrum), +1, p->batch, st, p->fft_wide);
+  for (int pass = 0; pass < 2; ++pass) {
+    const so3::FftArgs a = pass == 0 ? fft_pass_args(p, 0, samples, p->d_scratch) : fft_pass_args(p, 1, p->d_scratch, spectrum);
+    if (int rc = launch_fft(a, +1, p->batch, st, p->fft_wide)) return rc;
+  }
+  return SO3_OK;
 }
 
 int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream) {
@@ -814,9 +891,13 @@ int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream)
     return fail(SO3_ERR_INVALID, "fft_synthesis: buffers must not alias each other or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (int rc = launch_fft2d(p, -1, spectrum, samples, st); rc >= 0) return rc;
-  int rc = launch_fft(fft_pass_args(p, 2, spectrum, p->d_scratch), -1, p->batch, st, p->fft_wide);
-  if (rc) return rc;
-  return launch_fft(fft_pass_args(p, 3, p->d_scratch, samples), -1, p->batch, st, p->fft_wide);
+  for (int pass = 2; pass < 4; ++pass) {
+    const so3::FftArgs a = pass == 2 ? fft_pass_args(p, 2, spectrum, p->d_scratch) : fft_pass_args(p, 3, p->d_scratch, samples);
+    int rc = launch_fft_tma(p, a, -1, st);
+    if (rc < 0) rc = launch_fft(a, -1, p->batch, st, p->fft_wide);
+    if (rc) return rc;
+  }
+  return SO3_OK;
 }
 
 int so3_dwt_analysis(so3_plan_t p, const void* spectrum, void* coeffs, int64_t c0, int64_t c1, void* stream) {

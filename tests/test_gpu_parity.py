@@ -371,6 +371,23 @@ def test_one_pass_slice_fft_matches_two_pass(b, F):
     assert torch.equal(g1, g0)
 
 
+@pytest.mark.parametrize("b,F,mode", [(512, 1, 1), (128, 3, 2), (256, 1, 2)])
+def test_tma_fed_inverse_fft_matches_plain_passes(b, F, mode):
+    """fft_tma_kernel (TMA tensor loads of the strided chunk side, persistent teams; default at
+    2B = 1024, mode 2 = every size it supports) runs the plain pass's radix code: the inverse
+    FFT stage must be bit-identical to fft_pass_kernel, including ragged batches."""
+    n = 2 * b
+    gen = torch.Generator(device="cuda").manual_seed(7 + b)
+    spec = torch.randn(F * n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
+    p1, p0 = plan_for(b, batch=F), plan_for(b, batch=F)
+    p1.set_knob("fft_tma", mode)
+    p0.set_knob("fft_tma", 0)
+    g1, g0 = torch.empty_like(spec), torch.empty_like(spec)
+    so3.fft_synthesis(p1, spec, g1)
+    so3.fft_synthesis(p0, spec, g0)
+    assert torch.equal(torch.view_as_real(g1), torch.view_as_real(g0))
+
+
 def test_batched_dwt_knob_off_matches():
     b, F = 16, 8
     rng = np.random.default_rng(77)
