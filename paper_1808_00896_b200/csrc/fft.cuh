@@ -326,6 +326,63 @@ __global__ void __launch_bounds__(XB * N / 16, MINB) fft_pass_kernel(FftArgs a) 
   }
 }
 
+// Row-table passes of the sharded pipeline (K1b stores, K4a loads through the (m', m) -> row
+// table of the all-to-all layout).  The table entries of a CTA depend on y only, so a CTA keeps
+// its 16 entries per thread in registers and walks x-tiles blockIdx.x, + gridDim.x, ...: the
+// dependent table -> data load pair is paid once per CTA instead of once per tile (at G = 8
+// ranks the per-tile dependent load made K4a ~1.5x slower than the plain pass).
+template <int N, int XB, int SIGN>
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+    fft_tab_kernel(FftArgs a) {
+  extern __shared__ double2 smem[];
+  constexpr int TPR = N / 16;
+  const int tid = threadIdx.x;
+  const int xl = tid % XB, t = tid / XB;
+  const int y = blockIdx.y;
+  if (y == a.skip_y) return;
+  const long long f = blockIdx.z;
+  double2* row = smem + xl * RowLayout<N, XB>::SIZE;
+  int rin[16], rout[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int p = t + e * TPR;
+    rin[e] = a.tab_in ? (p != a.zero_p ? __ldg(&a.tab_in[(long long)y * N + p]) : -1) : p;
+    rout[e] = a.tab_out ? __ldg(&a.tab_out[(long long)y * N + p]) : p;
+  }
+  for (int xt = blockIdx.x; xt * XB < a.X; xt += gridDim.x) {
+    const int x = xt * XB + xl;
+    const bool xvalid = x < a.X;
+    double2 v[16];
+    if (a.tab_in) {
+      const double2* base = a.src + f * a.fs_in + x;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        v[e] = (xvalid && rin[e] >= 0) ? base[(long long)rin[e] * a.tabJ] : make_double2(0.0, 0.0);
+    } else {
+      const double2* src = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)x * a.sx_in;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int p = t + e * TPR;
+        v[e] = (!xvalid || p == a.zero_p) ? make_double2(0.0, 0.0) : src[(long long)p * a.sp_in];
+      }
+    }
+    fft_rows<N, SIGN>(v, t, a.tw, row);   // ends behind a barrier: the rows are free for the next tile
+    const double wx = (a.weight && xvalid) ? __ldg(&a.w[a.jbase + x]) : 1.0;
+    if (xvalid) {
+      if (a.tab_out) {
+        double2* tbase = a.dst + f * a.fs_out + x;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          if (rout[e] >= 0) tbase[(long long)rout[e] * a.tabJ] = make_double2(v[e].x * wx, v[e].y * wx);
+      } else {
+        double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)x * a.sx_out;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) dst[(long long)(t + e * TPR) * a.sp_out] = make_double2(v[e].x * wx, v[e].y * wx);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------------
 // One-pass 2-D transform of whole beta slices for N = 2B <= 64 (a slice is N*N complex128,
 // 64 KB at N = 64, so it fits in shared memory): the grid side moves through shared memory

@@ -172,12 +172,22 @@ struct so3_plan_s {
 
 namespace {
 
+int g_fft_tab_loop = 8;   // dev knob fft_tab_loop: x-tiles per CTA of the row-table passes (0: per-tile kernel)
+
 template <int N, int XB>
 int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
   const int threads = XB * N / 16;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
   dim3 grid((a.X + XB - 1) / XB, a.Y, batch);
   const bool tab = a.tab_in || a.tab_out;
+  if (tab && g_fft_tab_loop > 0) {
+    auto kt = sign > 0 ? so3::fft_tab_kernel<N, XB, +1> : so3::fft_tab_kernel<N, XB, -1>;
+    if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    grid.x = (grid.x + g_fft_tab_loop - 1) / g_fft_tab_loop;
+    kt<<<grid, threads, smem, st>>>(a);
+    SO3_CUDA(cudaGetLastError());
+    return SO3_OK;
+  }
   void (*k)(so3::FftArgs) = sign > 0 ? (tab ? so3::fft_pass_kernel<N, XB, +1, true> : so3::fft_pass_kernel<N, XB, +1, false>)
                                      : (tab ? so3::fft_pass_kernel<N, XB, -1, true> : so3::fft_pass_kernel<N, XB, -1, false>);
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -857,6 +867,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
   if (k == "fft_tma") { p->fft_tma = value; return SO3_OK; }
+  if (k == "fft_tab_loop") { g_fft_tab_loop = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
@@ -1019,7 +1030,9 @@ int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* st
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = launch_fft(shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st, p->fft_wide);
   if (rc) return rc;
-  return launch_fft(shard_pass_args(p, 3, p->d_scratch, slab), -1, 1, st, p->fft_wide);
+  const so3::FftArgs a3 = shard_pass_args(p, 3, p->d_scratch, slab);   // plain strides: TMA-fed when it applies
+  rc = launch_fft_tma(p, a3, -1, st);
+  return rc >= 0 ? rc : launch_fft(a3, -1, 1, st, p->fft_wide);
 }
 
 // Direct O(B^6) transforms (soft.py:212-256): closed-form Wigner functions, no plan.

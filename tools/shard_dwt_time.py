@@ -8,6 +8,9 @@ from paper_1808_00896_b200.distributed import NativeShardBackend, ShardMap
 b, world = int(sys.argv[1]), int(sys.argv[2])
 m = ShardMap(b, world)
 be = NativeShardBackend(b, world, 0)
+for kv in sys.argv[3:]:   # knobs, e.g. fft_tab_loop=0
+    k, v = kv.split("=")
+    so3._native.check(so3._native.lib().so3_plan_set_knob(be.handle, k.encode(), int(v)), "set_knob")
 C = so3.coeff_count(b)
 rng = np.random.default_rng(1)
 coef = torch.from_numpy(rng.standard_normal(C) + 1j * rng.standard_normal(C)).cuda()
