@@ -61,7 +61,8 @@ def emulate(b, world, grid, coeffs, chunks=1):
 
 
 @pytest.mark.parametrize("b,world,chunks", [(8, 2, 1), (16, 4, 1), (33, 2, 1), (64, 8, 1), (128, 4, 1),
-                                            (16, 2, 3), (64, 4, 4), (128, 8, 8), (5, 2, 6)])
+                                            (16, 2, 3), (64, 4, 4), (128, 8, 8), (5, 2, 6), (256, 2, 4),
+                                            (512, 8, 4)])
 def test_sharded_equals_single_gpu_bitwise(b, world, chunks):
     n = 2 * b
     rng = np.random.default_rng(b + world)
