@@ -126,7 +126,7 @@ int so3_dwt_analysis(so3_plan_t plan, const void* spectrum_dev, void* coeffs_dev
 int so3_dwt_synthesis(so3_plan_t plan, const void* coeffs_dev, void* spectrum_dev,
                       int64_t cluster_begin, int64_t cluster_end, void* stream);
 
-/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4) or SO3_DWT_SIMT (DFMA +
+/* DWT kernel family: SO3_DWT_MMA (default; FP64 DMMA m8n8k4 / m16n8k4) or SO3_DWT_SIMT (DFMA +
  * warp butterfly).  Same results to rounding. */
 #define SO3_DWT_MMA 0
 #define SO3_DWT_SIMT 1
@@ -135,7 +135,10 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * (synthesis beta indices per warp, 0 = default), "fft_xb" (FFT rows per CTA for
  * 2B in {256, 512, 1024}, 0 = default), "dwt_batch" (1 = dense-contraction DWT for batched
  * plans with 2B <= 64, 0 = per-function kernels), "fft_fused" (1 = one-pass 2-D slice FFT for
- * 2B <= 64, 0 = two passes).  Unknown names fail with SO3_ERR_INVALID. */
+ * 2B <= 64, 0 = two passes), "fft_tma" (1 = TMA-fed chunks-in FFT passes at 2B = 1024,
+ * 2 = also 2B = 256 and 512, 0 = off; bit-identical), "fft_tab_loop" (x-tiles per CTA of the
+ * sharded row-table FFT passes, 0 = one tile per CTA; process-wide).  Unknown names fail with
+ * SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */
