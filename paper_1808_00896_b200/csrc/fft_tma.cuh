@@ -154,4 +154,105 @@ __global__ void __launch_bounds__(TmaGeom<N>::G * TmaGeom<N>::TPG, 1)
   }
 }
 
+
+__device__ __forceinline__ void tensor_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tensor_store4(const CUtensorMap* map, int c0, int c1, int c2, int c3, const void* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src))
+               : "memory");
+}
+
+// One-pass 2-D slice transform (2B <= 64, fft2d_slice_kernel in fft.cuh) with the pair-major
+// side moved by the TMA.  For one beta index j, X[f][m'][m][j] is N*N elements 16 bytes wide
+// and N*16 bytes apart: as per-thread accesses every one is its own L1 wavefront (ncu: the
+// L1 data pipe at 64-68 %, MIO throttle 35-43 %).  Here one 4-D tensor copy moves the whole
+// slice: dims (j as 2 doubles, m', m, f) -- m' before m, so the shared box is [m][m'] and the
+// threads, consecutive in m', read / write it conflict-free.  Same radix code and order as
+// fft2d_slice_kernel: results are bit-identical (the forward also writes the unused Nyquist
+// row m' = B, which the DWT never reads).
+template <int N, int SIGN>
+__global__ void __launch_bounds__(N * N / 16, (N >= 64 ? 2 : 4))
+    fft2d_slice_tma_kernel(const __grid_constant__ CUtensorMap xmap, const double2* __restrict__ src,
+                           double2* __restrict__ dst, const double2* __restrict__ tw, const double* __restrict__ w,
+                           long long fstride, int nyq) {
+  constexpr int NT = N * N / 16, TPR = N / 16, SIZE = RowLayout<N, N>::SIZE;
+  extern __shared__ __align__(1024) double2 E[];   // N rows of SIZE (padded); the dense box at its start
+  uint64_t* bar = reinterpret_cast<uint64_t*>(E + N * SIZE);
+  const int j = blockIdx.x;
+  const int f = blockIdx.y;
+  const int tid = threadIdx.x, r = tid % N, t = tid / N;
+  const long long n = N;
+  double2* row = E + r * SIZE;
+  double2 v[16];
+  if (SIGN > 0) {
+    const double2* in = src + f * fstride;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + NT * q, i = idx / N, k = idx % N;
+      E[i * SIZE + pidx(k)] = in[((long long)i * n + j) * n + k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * TPR)];
+  } else {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(bar, N * N * sizeof(double2));
+      tensor_load4(E, &xmap, 2 * j, 0, 0, f, bar);
+    }
+    __syncthreads();   // the barrier is initialised before anyone waits on it
+    while (!mbar_try_wait(bar, 0)) {
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int m = t + e * TPR;
+      v[e] = (r == nyq || m == nyq) ? make_double2(0.0, 0.0) : E[m * N + r];   // box [m][m']
+    }
+  }
+  __syncthreads();   // every thread holds its inputs before the rows are reused for exchange
+  fft_rows<N, SIGN>(v, t, tw, row);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) E[(t + e * TPR) * SIZE + pidx(r)] = v[e];
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = row[pidx(t + e * TPR)];
+  __syncthreads();
+  fft_rows<N, SIGN>(v, t, tw, row);
+  if (SIGN > 0) {
+    // v[e] = S(m = t + TPR e, m' = r) * w_j -> the dense box [m][m'], one tensor store
+    const double wj = __ldg(&w[j]);
+    __syncthreads();   // the last exchange's rows are no longer read
+#pragma unroll
+    for (int e = 0; e < 16; ++e) E[(t + e * TPR) * N + r] = make_double2(v[e].x * wj, v[e].y * wj);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tensor_store4(&xmap, 2 * j, 0, 0, f, E);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  } else {
+    // v[e] = f(i = r, k = t + TPR e): through E for coalesced grid rows
+    double2* out = dst + f * fstride;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) row[pidx(t + e * TPR)] = v[e];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int idx = tid + NT * q, i = idx / N, k = idx % N;
+      out[((long long)i * n + j) * n + k] = E[i * SIZE + pidx(k)];
+    }
+  }
+}
+
 }  // namespace so3

@@ -290,8 +290,40 @@ int launch_fft(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int 
   }
 }
 
+EncodeTiledFn encode_tiled();
+
+// Slice transform with the pair-major side by TMA (fft_tma.cuh): tensor map over X with dims
+// (j as doubles, m', m, f) -- strides n^2, n, n^3 complex128 -- and box (2, N, N, 1).
+template <int N, int SIGN>
+int launch_fft2d_tma_t(const so3_plan_s* p, const void* src, void* dst, cudaStream_t st) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  const void* x = SIGN > 0 ? dst : src;
+  const cuuint64_t n = (cuuint64_t)N;
+  const cuuint64_t dims[4] = {2 * n, n, n, (cuuint64_t)p->batch};
+  const cuuint64_t strides[3] = {n * n * 16, n * 16, (cuuint64_t)p->ngrid * 16};
+  const cuuint32_t box[4] = {2, (cuuint32_t)N, (cuuint32_t)N, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<void*>(x), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;   // the plain slice kernel takes over
+  const size_t smem = (size_t)N * so3::RowLayout<N, N>::SIZE * sizeof(double2) + 16;
+  auto k = so3::fft2d_slice_tma_kernel<N, SIGN>;
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(N, p->batch), N * N / 16, smem, st>>>(map, static_cast<const double2*>(src), static_cast<double2*>(dst),
+                                                 p->d_tw, p->d_w, p->ngrid, p->B);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 template <int N, int SIGN>
 int launch_fft2d_t(const so3_plan_s* p, const void* src, void* dst, cudaStream_t st) {
+  if (p->fft_tma) {
+    const int rc = launch_fft2d_tma_t<N, SIGN>(p, src, dst, st);
+    if (rc >= 0) return rc;
+  }
   const size_t smem = (size_t)N * so3::RowLayout<N, N>::SIZE * sizeof(double2);
   auto k = so3::fft2d_slice_kernel<N, SIGN>;
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
