@@ -384,12 +384,13 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     # (read) once; below the FP64 ridge (small B) the DWT is HBM-bound
     dwt_bytes = 16.0 * F * (n ** 3 + C)
     dwt_bound = "fp64" if fl / dwt_bytes >= p64 / bw else "hbm"
-    fused = n in (16, 32, 64)   # one-pass slice FFT (fft2d_slice_kernel)
+    fused = n in (16, 32, 64)   # one-pass slice FFT (fft2d_slice_tma_kernel: pair-major side by TMA)
     kernel_of = {
         "dwt_analysis": "dwt_analysis_batch_reg_kernel" if (F >= 2 and n <= 64) else "dwt_analysis_mma_cta_kernel",
         "dwt_synthesis": "dwt_synthesis_batch_kernel" if (F >= 2 and n <= 64) else "dwt_synthesis_mma_kernel",
-        "fft_analysis": "fft2d_slice_kernel" if fused else "fft_pass_kernel x2",
-        "fft_synthesis": "fft2d_slice_kernel" if fused else "fft_pass_kernel x2",
+        "fft_analysis": "fft2d_slice_tma_kernel" if fused else "fft_pass_kernel x2",
+        "fft_synthesis": "fft2d_slice_tma_kernel" if fused else
+                         ("fft_tma_kernel x2" if n == 1024 else "fft_pass_kernel x2"),
     }
     stages = {}
     for nm in stage_names:
