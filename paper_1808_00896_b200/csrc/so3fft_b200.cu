@@ -233,7 +233,7 @@ template <int N, int SIGN>
 int launch_fft_tma_t(const so3::FftArgs& a, int batch, int device, cudaStream_t st) {
   using TG = so3::TmaGeom<N>;
   EncodeTiledFn enc = encode_tiled();
-  if (!enc) return fail(SO3_ERR_CUDA, "cuTensorMapEncodeTiled is not available from the driver");
+  if (!enc) return -1;   // no driver entry point: the plain pass takes over
   const int plo = N < 256 ? N : 256, phi = N / plo;
   const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
   const cuuint64_t strides[4] = {(cuuint64_t)a.sp_in * 16, (cuuint64_t)plo * a.sp_in * 16, (cuuint64_t)a.sy_in * 16,
@@ -244,7 +244,7 @@ int launch_fft_tma_t(const so3::FftArgs& a, int batch, int device, cudaStream_t 
   const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(a.src), dims, strides, box, es,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(SO3_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  if (r != CUDA_SUCCESS) return -1;   // shape the tensor map cannot describe: the plain pass takes over
   so3::FftTmaArgs t;
   t.X = a.X; t.Y = a.Y; t.skip_y = a.skip_y; t.zero_p = a.zero_p;
   t.ntiles = (long long)(a.X / TG::XB) * (a.Y - (a.skip_y >= 0 ? 1 : 0)) * batch;
