@@ -135,8 +135,9 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * (synthesis beta indices per warp, 0 = default), "fft_xb" (FFT rows per CTA for
  * 2B in {256, 512, 1024}, 0 = default), "dwt_batch" (1 = dense-contraction DWT for batched
  * plans with 2B <= 64, 0 = per-function kernels), "fft_fused" (1 = one-pass 2-D slice FFT for
- * 2B <= 64, 0 = two passes), "fft_tma" (1 = TMA-fed chunks-in FFT passes at 2B = 1024,
- * 2 = also 2B = 256 and 512, 0 = off; bit-identical), "fft_tab_loop" (x-tiles per CTA of the
+ * 2B <= 64, 0 = two passes), "fft_tma" (1 = FFT tiles move their strided side by TMA tensor
+ * copies: passes at 2B in {256, 512, 1024} and the one-pass slices; 0 = per-thread loads and
+ * stores; bit-identical), "fft_tab_loop" (x-tiles per CTA of the
  * sharded row-table FFT passes, 0 = one tile per CTA; process-wide).  Unknown names fail with
  * SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);

@@ -1,38 +1,25 @@
-// Chunks-in torus FFT pass (K4a, K4b: the inverse direction) fed by the Tensor Memory
-// Accelerator (sm_100a): the same rows, radix code and exchange layout as fft_pass_kernel
-// (fft.cuh), so results are bit-identical, but the strided chunk side of every tile arrives by
-// one asynchronous 5-D tensor copy instead of 16 per-thread loads.
+// TMA-fed torus FFT kernels (sm_100a).  The strided side of every FFT tile -- 16-byte
+// elements, one per (row, point), N*16 or more bytes apart -- moves by ONE tensor copy
+// (cp.async.bulk.tensor) through shared memory instead of per-thread 16-byte loads / stores,
+// each of which is its own L1 wavefront and LSU queue entry:
 //
-// One persistent CTA per SM holds G thread teams of XB*N/16 threads and a ring of S > G
-// shared-memory slots of one tile (XB = 4 rows of N complex128) each.  Team g takes the CTA's
-// local tiles g, g + G, ...; tile k lives in slot k % S.  While the teams transform their
-// tiles, the TMA fills the spare slots with the next tiles, so a tile's HBM latency is paid
-// under another tile's arithmetic instead of by registers held across the load.  Per tile:
+//   fft_pass_tstore_kernel   rows-in passes (K1a, K1b): chunk-side outputs staged [p][x] in the
+//                            exchange rows, one 5-D tensor store per tile
+//   fft_pass_tload_kernel    chunks-in passes (K4a, K4b): one 5-D tensor load per tile into the
+//                            exchange rows, behind an mbarrier with expect_tx
+//   fft2d_slice_tma_kernel   one-pass slices (2B <= 64): the pair-major side of a beta slice as
+//                            one 4-D tensor load / store
 //
-//   full[k % S] (mbarrier, expect_tx)  <-  tensor load of tile k: box (2 XB doubles, p mod 256,
-//                                          p / 256, 1, 1), staged [p][x] (64 bytes per p)
-//   team: slot -> registers, fft_rows with the exchange rows in the slot itself (one named
-//         barrier per team), then one thread issues the load of tile k + S into the slot and
-//         the team stores its rows from registers.
-//
-// Measured at 2B = 1024 (B200): 14.6 ms vs 15.2 ms per inverse FFT stage.  The rows-in passes
-// (K1a, K1b) were also built this way -- 1-D bulk row loads, tensor or register stores -- and
-// were slower than the plain kernel (17.8-18.6 ms vs 14.7 ms per forward stage), as were both
-// directions at 2B = 256 and 512, so only this pass uses the TMA.  The tensor map
-// must not promote L2 fills (256-byte promotion over-fetched 10 GB per pass).
+// The radix code (fft_rows) and its order are those of the plain kernels, so results are
+// bit-identical.  Tensor maps are built per launch on the host (so3fft_b200.cu) with no L2
+// promotion (256-byte promotion over-fetched 10 GB per pass at 2B = 1024).  A persistent
+// variant (two teams per CTA, a 3-slot smem ring, loads issued one tile ahead) was slower than
+// one tile per CTA with the tensor load: 15.0 vs 12.5 ms per inverse stage at 2B = 1024.
 #pragma once
 #include <cuda.h>
 #include "fft.cuh"
 
 namespace so3 {
-
-struct FftTmaArgs {
-  int X, Y, skip_y, zero_p;
-  long long ntiles;          // (X / XB) * (rows y other than skip_y) * batch
-  double2* rows_dst;         // output rows: element (x, y, p, f) at f*fs + y*sy + x*sx + p
-  long long fs, sy, sx;
-  const double2* tw;
-};
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -59,101 +46,6 @@ __device__ __forceinline__ void tensor_load5(void* dst, const CUtensorMap* map, 
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(bar))
       : "memory");
 }
-
-struct TeamSync {
-  int id, count;
-  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
-};
-
-template <int N>
-struct TmaGeom {
-  static constexpr int XB = 4;
-  static constexpr int TPG = XB * N / 16;                         // threads per team
-  static constexpr int G = N >= 1024 ? 2 : N >= 512 ? 4 : 8;       // teams per CTA (512 threads)
-  static constexpr int SLOT = XB * RowLayout<N, XB>::SIZE;         // complex128 per slot (exchange rows)
-  static constexpr int S = N >= 1024 ? 3 : N >= 512 ? 6 : 12;      // ring slots (> G, ~210 KB)
-  static constexpr size_t SMEM = (size_t)S * SLOT * sizeof(double2);
-  static_assert((SLOT * sizeof(double2)) % 128 == 0, "slots must stay 128-byte aligned for the tensor copies");
-};
-
-template <int N, int SIGN>
-__global__ void __launch_bounds__(TmaGeom<N>::G * TmaGeom<N>::TPG, 1)
-    fft_tma_kernel(const __grid_constant__ CUtensorMap tmap, FftTmaArgs a) {
-  using TG = TmaGeom<N>;
-  constexpr int XB = TG::XB, TPG = TG::TPG, G = TG::G, S = TG::S, SLOT = TG::SLOT, TPR = N / 16;
-  constexpr uint32_t TILE_BYTES = XB * N * sizeof(double2);
-  extern __shared__ __align__(1024) double2 smem[];
-  __shared__ uint64_t full[S];
-  __shared__ volatile long long issued[S];   // local tile whose load was last issued into slot s
-  const int tid = threadIdx.x, team = tid / TPG, lt = tid % TPG;
-  const int xl = lt % XB, t = lt / XB;
-  const int XT = a.X / XB;
-  const int Yv = a.Y - (a.skip_y >= 0 ? 1 : 0);
-  const long long per_f = (long long)XT * Yv;
-
-  auto coords = [&](long long tile, int& xt, int& y, int& f) {
-    f = (int)(tile / per_f);
-    const long long r = tile - (long long)f * per_f;
-    y = (int)(r / XT);
-    xt = (int)(r - (long long)y * XT);
-    if (a.skip_y >= 0 && y >= a.skip_y) ++y;
-  };
-  // one thread: the tensor load of local tile k into slot k % S
-  auto issue = [&](long long k) {
-    const long long tile = blockIdx.x + k * gridDim.x;
-    if (tile >= a.ntiles) return;
-    int xt, y, f;
-    coords(tile, xt, y, f);
-    const int sl = (int)(k % S);
-    mbar_expect_tx(&full[sl], TILE_BYTES);
-    tensor_load5(smem + (size_t)sl * SLOT, &tmap, 2 * xt * XB, 0, 0, y, f, &full[sl]);
-    issued[sl] = k;
-  };
-
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      issued[s] = -1;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int k = 0; k < S; ++k) issue(k);
-
-  const TeamSync sync{1 + team, TPG};
-  for (long long k = team; blockIdx.x + k * gridDim.x < a.ntiles; k += G) {
-    const long long tile = blockIdx.x + k * gridDim.x;
-    int xt, y, f;
-    coords(tile, xt, y, f);
-    const int sl = (int)(k % S);
-    double2* slot = smem + (size_t)sl * SLOT;
-    // the load of tile k must have been ISSUED before its parity is tested: an earlier phase
-    // of the same slot has the same parity
-    while (issued[sl] != k) {
-    }
-    while (!mbar_try_wait(&full[sl], (uint32_t)((k / S) & 1))) {
-    }
-    double2 v[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const int p = t + e * TPR;
-      v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : slot[p * XB + xl];   // [p][x] box
-    }
-    sync();   // the whole tile is in registers before the slot becomes the exchange rows
-    fft_rows<N, SIGN>(v, t, a.tw, slot + xl * RowLayout<N, XB>::SIZE, sync);
-    // the last exchange ended with a team barrier: the slot is free, refill it now and store
-    // the rows straight from registers (128-byte lines per quarter warp)
-    if (lt == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(k + S);
-    }
-    double2* out = a.rows_dst + f * a.fs + (long long)y * a.sy + (long long)(xt * XB + xl) * a.sx;
-#pragma unroll
-    for (int e = 0; e < 16; ++e) out[t + e * TPR] = v[e];
-  }
-}
-
 
 __device__ __forceinline__ void tensor_load4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
                                              uint64_t* bar) {
@@ -253,6 +145,88 @@ __global__ void __launch_bounds__(N * N / 16, (N >= 64 ? 2 : 4))
       out[((long long)i * n + j) * n + k] = E[i * SIZE + pidx(k)];
     }
   }
+}
+
+
+__device__ __forceinline__ void tensor_store5(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                              const void* src) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_addr(src))
+               : "memory");
+}
+
+// Rows-in pass (K1a, K1b) as fft_pass_kernel, but the chunk-side outputs leave by ONE tensor
+// store per tile: staged [p][x] in the exchange rows (conflict-free for tid = xl + XB t), box
+// (2 XB doubles, p mod 256, p / 256, 1, 1).  The per-thread 64-byte chunk stores filled the
+// LSU queue (lg_throttle 12.7 % of the plain pass's stalls).
+template <int N, int XB, int SIGN>
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+    fft_pass_tstore_kernel(const __grid_constant__ CUtensorMap omap, FftArgs a) {
+  extern __shared__ __align__(1024) double2 smem[];
+  constexpr int TPR = N / 16;
+  const int tid = threadIdx.x;
+  const int xl = tid % XB, t = tid / XB;
+  const int y = blockIdx.y;
+  const int xt = blockIdx.x;
+  const int x = xt * XB + xl;
+  if (y == a.skip_y) return;   // uniform per CTA
+  const long long f = blockIdx.z;
+  const double2* src = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)x * a.sx_in;
+  double2* row = smem + xl * RowLayout<N, XB>::SIZE;
+  double2 v[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int p = t + e * TPR;
+    v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : src[p];
+  }
+  fft_rows<N, SIGN>(v, t, a.tw, row);   // ends behind a barrier: the rows are free
+  const double wx = a.weight ? __ldg(&a.w[a.jbase + x]) : 1.0;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) smem[(t + e * TPR) * XB + xl] = make_double2(v[e].x * wx, v[e].y * wx);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    tensor_store5(&omap, 2 * xt * XB, 0, 0, y, (int)f, smem);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
+// Chunks-in pass (K4a, K4b) as fft_pass_kernel, with the tile's chunk side arriving by ONE
+// tensor load into the exchange rows (mbarrier after the rows) instead of 16 per-thread loads.
+template <int N, int XB, int SIGN>
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+    fft_pass_tload_kernel(const __grid_constant__ CUtensorMap imap, FftArgs a) {
+  extern __shared__ __align__(1024) double2 smem[];
+  constexpr int TPR = N / 16;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + XB * RowLayout<N, XB>::SIZE);
+  const int tid = threadIdx.x;
+  const int xl = tid % XB, t = tid / XB;
+  const int y = blockIdx.y;
+  const int xt = blockIdx.x;
+  const int x = xt * XB + xl;
+  if (y == a.skip_y) return;   // uniform per CTA
+  const long long f = blockIdx.z;
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, XB * N * sizeof(double2));
+    tensor_load5(smem, &imap, 2 * xt * XB, 0, 0, y, (int)f, bar);
+  }
+  __syncthreads();
+  while (!mbar_try_wait(bar, 0)) {
+  }
+  double2 v[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int p = t + e * TPR;
+    v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : smem[p * XB + xl];
+  }
+  __syncthreads();   // the box is in registers before the rows are reused for the exchange
+  fft_rows<N, SIGN>(v, t, a.tw, smem + xl * RowLayout<N, XB>::SIZE);
+  double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)x * a.sx_out;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) dst[t + e * TPR] = v[e];
 }
 
 }  // namespace so3

@@ -164,7 +164,7 @@ struct so3_plan_s {
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
-  int fft_tma = 1;    // 2B = 1024: TMA-fed chunks-in passes (fft_tma.cuh); 2: also 2B = 256, 512
+  int fft_tma = 1;    // TMA-fed FFT kernels (fft_tma.cuh): passes at 2B in {256, 512, 1024}, one-pass slices
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
 };
 
@@ -227,40 +227,8 @@ EncodeTiledFn encode_tiled() {
 
 // TMA-fed pass (fft_tma.cuh): RI passes read rows / write chunks, CI passes the reverse.  The
 // chunk side is described by a 5-D tensor map over (x as doubles, p mod 256, p / 256, y, f).
-// TMA-fed chunks-in pass (fft_tma.cuh, K4a / K4b).  The chunk side is described by a 5-D
-// tensor map over (x as doubles, p mod 256, p / 256, y, f), box (8, p_lo, p_hi, 1, 1).
 template <int N, int SIGN>
-int launch_fft_tma_t(const so3::FftArgs& a, int batch, int device, cudaStream_t st) {
-  using TG = so3::TmaGeom<N>;
-  EncodeTiledFn enc = encode_tiled();
-  if (!enc) return -1;   // no driver entry point: the plain pass takes over
-  const int plo = N < 256 ? N : 256, phi = N / plo;
-  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
-  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_in * 16, (cuuint64_t)plo * a.sp_in * 16, (cuuint64_t)a.sy_in * 16,
-                                 (cuuint64_t)std::max<long long>(a.fs_in, 1) * 16};
-  const cuuint32_t box[5] = {(cuuint32_t)(2 * TG::XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
-  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  CUtensorMap map;
-  const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(a.src), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return -1;   // shape the tensor map cannot describe: the plain pass takes over
-  so3::FftTmaArgs t;
-  t.X = a.X; t.Y = a.Y; t.skip_y = a.skip_y; t.zero_p = a.zero_p;
-  t.ntiles = (long long)(a.X / TG::XB) * (a.Y - (a.skip_y >= 0 ? 1 : 0)) * batch;
-  t.rows_dst = a.dst;
-  t.fs = a.fs_out; t.sy = a.sy_out; t.sx = a.sx_out;
-  t.tw = a.tw;
-  auto k = so3::fft_tma_kernel<N, SIGN>;
-  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
-  int sms = 0;
-  SO3_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  const long long grid = std::min<long long>(sms, t.ntiles);
-  if (grid < 1) return SO3_OK;
-  k<<<(unsigned)grid, TG::G * TG::TPG, TG::SMEM, st>>>(map, t);
-  SO3_CUDA(cudaGetLastError());
-  return SO3_OK;
-}
+auto sign_kernel_tstore() { return so3::fft_pass_tstore_kernel<N, 4, SIGN>; }
 
 // returns -1 when the TMA pass does not apply (row tables, odd sizes, knob off)
 int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st);
@@ -345,18 +313,74 @@ int launch_fft2d(const so3_plan_s* p, int sign, const void* src, void* dst, cuda
   }
 }
 
+// Rows-in pass with a TMA tensor store of each tile's chunk side (fft_tma.cuh).
+template <int N, int SIGN>
+int launch_fft_tstore_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
+  constexpr int XB = 4;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  const int plo = N < 256 ? N : 256, phi = N / plo;
+  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_out * 16, (cuuint64_t)plo * a.sp_out * 16, (cuuint64_t)a.sy_out * 16,
+                                 (cuuint64_t)std::max<long long>(a.fs_out, 1) * 16};
+  const cuuint32_t box[5] = {(cuuint32_t)(2 * XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.dst, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
+  auto k = sign_kernel_tstore<N, SIGN>();
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+// Chunks-in pass with a TMA tensor load of each tile's chunk side (fft_tma.cuh).
+template <int N, int SIGN>
+int launch_fft_tload_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
+  constexpr int XB = 4;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  const int plo = N < 256 ? N : 256, phi = N / plo;
+  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_in * 16, (cuuint64_t)plo * a.sp_in * 16, (cuuint64_t)a.sy_in * 16,
+                                 (cuuint64_t)std::max<long long>(a.fs_in, 1) * 16};
+  const cuuint32_t box[5] = {(cuuint32_t)(2 * XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(a.src), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  auto k = SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1> : so3::fft_pass_tload_kernel<N, XB, -1>;
+  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st) {
-  // chunks-in passes only (K4a, K4b); measured faster than fft_pass_kernel at 2B = 1024 only
-  // (fft_tma = 2 enables 2B = 256 and 512 as well, for measurements)
-  if (!p->fft_tma || p->fft_wide || a.tab_in || a.tab_out || a.X % 4 || a.weight) return -1;
-  if (a.sp_in == 1 || a.sx_in != 1 || a.sp_out != 1) return -1;
-  if (a.n != 1024 && p->fft_tma < 2) return -1;
-  switch (a.n) {
-    case 256: return sign > 0 ? launch_fft_tma_t<256, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<256, -1>(a, p->batch, p->device, st);
-    case 512: return sign > 0 ? launch_fft_tma_t<512, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<512, -1>(a, p->batch, p->device, st);
-    case 1024: return sign > 0 ? launch_fft_tma_t<1024, +1>(a, p->batch, p->device, st) : launch_fft_tma_t<1024, -1>(a, p->batch, p->device, st);
-    default: return -1;
+  // plain-stride passes at 2B in {256, 512, 1024}: rows-in -> TMA chunk stores, chunks-in -> TMA chunk loads
+  if (!p->fft_tma || p->fft_wide || a.tab_in || a.tab_out || a.X % 4) return -1;
+  if (a.n != 256 && a.n != 512 && a.n != 1024) return -1;
+  if (a.sp_in == 1 && a.sx_out == 1) {
+    switch (a.n) {
+      case 256: return sign > 0 ? launch_fft_tstore_t<256, +1>(a, p->batch, st) : launch_fft_tstore_t<256, -1>(a, p->batch, st);
+      case 512: return sign > 0 ? launch_fft_tstore_t<512, +1>(a, p->batch, st) : launch_fft_tstore_t<512, -1>(a, p->batch, st);
+      default: return sign > 0 ? launch_fft_tstore_t<1024, +1>(a, p->batch, st) : launch_fft_tstore_t<1024, -1>(a, p->batch, st);
+    }
   }
+  if (a.sp_in != 1 && a.sx_in == 1 && a.sp_out == 1 && !a.weight) {
+    switch (a.n) {
+      case 256: return sign > 0 ? launch_fft_tload_t<256, +1>(a, p->batch, st) : launch_fft_tload_t<256, -1>(a, p->batch, st);
+      case 512: return sign > 0 ? launch_fft_tload_t<512, +1>(a, p->batch, st) : launch_fft_tload_t<512, -1>(a, p->batch, st);
+      default: return sign > 0 ? launch_fft_tload_t<1024, +1>(a, p->batch, st) : launch_fft_tload_t<1024, -1>(a, p->batch, st);
+    }
+  }
+  return -1;
 }
 
 // The four passes (see fft.cuh).  n = 2B; all strides in complex128 units.
@@ -923,7 +947,9 @@ int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* st
   if (int rc = launch_fft2d(p, +1, samples, spectrum, st); rc >= 0) return rc;
   for (int pass = 0; pass < 2; ++pass) {
     const so3::FftArgs a = pass == 0 ? fft_pass_args(p, 0, samples, p->d_scratch) : fft_pass_args(p, 1, p->d_scratch, spectrum);
-    if (int rc = launch_fft(a, +1, p->batch, st, p->fft_wide)) return rc;
+    int rc = launch_fft_tma(p, a, +1, st);
+    if (rc < 0) rc = launch_fft(a, +1, p->batch, st, p->fft_wide);
+    if (rc) return rc;
   }
   return SO3_OK;
 }
@@ -1018,7 +1044,9 @@ int so3_ifsoft_host(so3_plan_t p, const void* coeffs_host, void* samples_host, v
 int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(slab); CHECK_PTR(send);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = launch_fft(shard_pass_args(p, 0, slab, p->d_scratch), +1, 1, st, p->fft_wide);
+  const so3::FftArgs a0 = shard_pass_args(p, 0, slab, p->d_scratch);   // plain strides: TMA-fed when it applies
+  int rc = launch_fft_tma(p, a0, +1, st);
+  if (rc < 0) rc = launch_fft(a0, +1, 1, st, p->fft_wide);
   if (rc) return rc;
   return launch_fft(shard_pass_args(p, 1, p->d_scratch, send), +1, 1, st, p->fft_wide);
 }

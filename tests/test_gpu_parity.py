@@ -371,21 +371,47 @@ def test_one_pass_slice_fft_matches_two_pass(b, F):
     assert torch.equal(g1, g0)
 
 
-@pytest.mark.parametrize("b,F,mode", [(512, 1, 1), (128, 3, 2), (256, 1, 2)])
-def test_tma_fed_inverse_fft_matches_plain_passes(b, F, mode):
-    """fft_tma_kernel (TMA tensor loads of the strided chunk side, persistent teams; default at
-    2B = 1024, mode 2 = every size it supports) runs the plain pass's radix code: the inverse
-    FFT stage must be bit-identical to fft_pass_kernel, including ragged batches."""
+@pytest.mark.parametrize("b,F", [(512, 1), (128, 3), (256, 1)])
+def test_tma_fed_fft_passes_match_plain_passes(b, F):
+    """fft_pass_tstore_kernel (rows-in passes: chunk side out by one TMA tensor store) and
+    fft_pass_tload_kernel (chunks-in passes: chunk side in by one tensor load) run the plain
+    pass's radix code: both FFT stages must be bit-identical to fft_pass_kernel (fft_tma = 0),
+    including ragged batches."""
     n = 2 * b
     gen = torch.Generator(device="cuda").manual_seed(7 + b)
-    spec = torch.randn(F * n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
+    x = torch.randn(F * n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
     p1, p0 = plan_for(b, batch=F), plan_for(b, batch=F)
-    p1.set_knob("fft_tma", mode)
     p0.set_knob("fft_tma", 0)
-    g1, g0 = torch.empty_like(spec), torch.empty_like(spec)
-    so3.fft_synthesis(p1, spec, g1)
-    so3.fft_synthesis(p0, spec, g0)
+    s1, s0 = torch.zeros_like(x), torch.zeros_like(x)
+    so3.fft_analysis(p1, x, s1)
+    so3.fft_analysis(p0, x, s0)
+    assert torch.equal(torch.view_as_real(s1), torch.view_as_real(s0))
+    del s1, s0
+    g1, g0 = torch.empty_like(x), torch.empty_like(x)
+    so3.fft_synthesis(p1, x, g1)
+    so3.fft_synthesis(p0, x, g0)
     assert torch.equal(torch.view_as_real(g1), torch.view_as_real(g0))
+
+
+@pytest.mark.parametrize("b,F", [(8, 3), (16, 5), (32, 4), (32, 1)])
+def test_tma_slice_fft_matches_plain_slice_kernel(b, F):
+    """fft2d_slice_tma_kernel (pair-major side by one 4-D tensor copy) vs fft2d_slice_kernel:
+    bit-identical (the TMA forward also writes the unused Nyquist row m' = B)."""
+    n = 2 * b
+    rng = np.random.default_rng(43 + b)
+    x = torch.from_numpy(rng.standard_normal(F * n ** 3) + 1j * rng.standard_normal(F * n ** 3)).cuda()
+    p1, p0 = plan_for(b, batch=F), plan_for(b, batch=F)
+    p0.set_knob("fft_tma", 0)
+    s1, s0 = torch.zeros_like(x), torch.zeros_like(x)
+    so3.fft_analysis(p1, x, s1)
+    so3.fft_analysis(p0, x, s0)
+    keep = torch.ones(F, n, n, n, dtype=torch.bool, device="cuda")
+    keep[:, b] = False
+    assert torch.equal(s1.view(F, n, n, n)[keep], s0.view(F, n, n, n)[keep])
+    g1, g0 = torch.empty_like(x), torch.empty_like(x)
+    so3.fft_synthesis(p1, x, g1)
+    so3.fft_synthesis(p0, x, g0)
+    assert torch.equal(g1, g0)
 
 
 def test_batched_dwt_knob_off_matches():
