@@ -3,10 +3,12 @@
 // (cp.async.bulk.tensor) through shared memory instead of per-thread 16-byte loads / stores,
 // each of which is its own L1 wavefront and LSU queue entry:
 //
-//   fft_pass_tstore_kernel   rows-in passes (K1a, K1b): chunk-side outputs staged [p][x] in the
-//                            exchange rows, one 5-D tensor store per tile
+//   fft_pass_tstore_kernel   rows-in passes (K1a, K1b): the XB input rows by 1-D bulk copies
+//                            (cp.async.bulk) into the exchange rows, chunk-side outputs staged
+//                            [p][x] there and sent by one 5-D tensor store per tile
 //   fft_pass_tload_kernel    chunks-in passes (K4a, K4b): one 5-D tensor load per tile into the
-//                            exchange rows, behind an mbarrier with expect_tx
+//                            exchange rows behind an mbarrier with expect_tx; rows out by 1-D
+//                            bulk stores (2B >= 512) or from registers
 //   fft2d_slice_tma_kernel   one-pass slices (2B <= 64): the pair-major side of a beta slice as
 //                            one 4-D tensor load / store
 //
@@ -159,11 +161,11 @@ __device__ __forceinline__ void tensor_store5(const CUtensorMap* map, int c0, in
 // store per tile: staged [p][x] in the exchange rows (conflict-free for tid = xl + XB t), box
 // (2 XB doubles, p mod 256, p / 256, 1, 1).  The per-thread 64-byte chunk stores filled the
 // LSU queue (lg_throttle 12.7 % of the plain pass's stalls).
-template <int N, int XB, int SIGN>
+template <int N, int XB, int SIGN, bool BULKIN = false>
 __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
     fft_pass_tstore_kernel(const __grid_constant__ CUtensorMap omap, FftArgs a) {
   extern __shared__ __align__(1024) double2 smem[];
-  constexpr int TPR = N / 16;
+  constexpr int TPR = N / 16, SIZE = RowLayout<N, XB>::SIZE;
   const int tid = threadIdx.x;
   const int xl = tid % XB, t = tid / XB;
   const int y = blockIdx.y;
@@ -172,12 +174,39 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
   if (y == a.skip_y) return;   // uniform per CTA
   const long long f = blockIdx.z;
   const double2* src = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)x * a.sx_in;
-  double2* row = smem + xl * RowLayout<N, XB>::SIZE;
+  double2* row = smem + xl * SIZE;
   double2 v[16];
+  if constexpr (BULKIN) {
+    // the XB input rows by 1-D bulk copies into the exchange rows (row stride SIZE = 2 mod 8
+    // 16-byte units: the reads below are conflict-free)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + XB * SIZE);
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(bar, XB * N * sizeof(double2));
+      const double2* r0 = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)xt * XB * a.sx_in;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) {
-    const int p = t + e * TPR;
-    v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : src[p];
+      for (int r = 0; r < XB; ++r)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_addr(smem + r * SIZE)),
+                     "l"(r0 + r * a.sx_in), "r"((uint32_t)(N * sizeof(double2))), "r"(smem_addr(bar))
+                     : "memory");
+    }
+    __syncthreads();
+    while (!mbar_try_wait(bar, 0)) {
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : row[p];
+    }
+    __syncthreads();   // the rows are in registers before the exchange reuses them
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : src[p];
+    }
   }
   fft_rows<N, SIGN>(v, t, a.tw, row);   // ends behind a barrier: the rows are free
   const double wx = a.weight ? __ldg(&a.w[a.jbase + x]) : 1.0;
@@ -194,7 +223,7 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
 
 // Chunks-in pass (K4a, K4b) as fft_pass_kernel, with the tile's chunk side arriving by ONE
 // tensor load into the exchange rows (mbarrier after the rows) instead of 16 per-thread loads.
-template <int N, int XB, int SIGN>
+template <int N, int XB, int SIGN, bool BULKOUT = false>
 __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
     fft_pass_tload_kernel(const __grid_constant__ CUtensorMap imap, FftArgs a) {
   extern __shared__ __align__(1024) double2 smem[];
@@ -224,9 +253,28 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
   }
   __syncthreads();   // the box is in registers before the rows are reused for the exchange
   fft_rows<N, SIGN>(v, t, a.tw, smem + xl * RowLayout<N, XB>::SIZE);
-  double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)x * a.sx_out;
+  if constexpr (BULKOUT) {
+    // rows staged in the exchange rows (stride SIZE, conflict-free) and stored by 1-D bulk copies
+    double2* row = smem + xl * RowLayout<N, XB>::SIZE;
 #pragma unroll
-  for (int e = 0; e < 16; ++e) dst[t + e * TPR] = v[e];
+    for (int e = 0; e < 16; ++e) row[t + e * TPR] = v[e];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      double2* d0 = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)xt * XB * a.sx_out;
+#pragma unroll
+      for (int r = 0; r < XB; ++r)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d0 + r * a.sx_out),
+                     "r"(smem_addr(smem + r * RowLayout<N, XB>::SIZE)), "r"((uint32_t)(N * sizeof(double2)))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+  } else {
+    double2* dst = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)x * a.sx_out;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) dst[t + e * TPR] = v[e];
+  }
 }
 
 }  // namespace so3

@@ -227,6 +227,9 @@ EncodeTiledFn encode_tiled() {
 
 // TMA-fed pass (fft_tma.cuh): RI passes read rows / write chunks, CI passes the reverse.  The
 // chunk side is described by a 5-D tensor map over (x as doubles, p mod 256, p / 256, y, f).
+int g_fft_bulkout = -1; // dev knob fft_bulkout: chunks-in passes store their rows by 1-D bulk copies (-1: 2B >= 512)
+int g_fft_bulkin = 1;   // dev knob fft_bulkin: rows-in passes also load their rows by 1-D bulk copies
+
 template <int N, int SIGN>
 auto sign_kernel_tstore() { return so3::fft_pass_tstore_kernel<N, 4, SIGN>; }
 
@@ -329,8 +332,9 @@ int launch_fft_tstore_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.dst, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
-  auto k = sign_kernel_tstore<N, SIGN>();
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  auto k = g_fft_bulkin ? (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1, true> : so3::fft_pass_tstore_kernel<N, XB, -1, true>)
+                        : sign_kernel_tstore<N, SIGN>();
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
   SO3_CUDA(cudaGetLastError());
@@ -355,7 +359,9 @@ int launch_fft_tload_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
-  auto k = SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1> : so3::fft_pass_tload_kernel<N, XB, -1>;
+  const bool bulkout = g_fft_bulkout < 0 ? N >= 512 : g_fft_bulkout != 0;
+  auto k = bulkout ? (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1, true> : so3::fft_pass_tload_kernel<N, XB, -1, true>)
+                         : (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1> : so3::fft_pass_tload_kernel<N, XB, -1>);
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
   SO3_CUDA(cudaGetLastError());
@@ -924,6 +930,8 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
   if (k == "fft_tma") { p->fft_tma = value; return SO3_OK; }
   if (k == "fft_tab_loop") { g_fft_tab_loop = value; return SO3_OK; }
+  if (k == "fft_bulkin") { g_fft_bulkin = value; return SO3_OK; }
+  if (k == "fft_bulkout") { g_fft_bulkout = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
