@@ -277,4 +277,91 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
   }
 }
 
+// Row-table passes of the sharded pipeline (fft_tab_kernel in fft.cuh) with the plain-strided
+// side moved by 1-D bulk copies: K1b (table on the output) loads its XB input rows by bulk
+// copies, K4a (table on the input) stores its XB output rows by bulk copies.  The table side
+// stays per thread (its 64-byte chunks go to / come from arbitrary rows of the all-to-all
+// buffer).  A CTA keeps its table entries in registers and walks x-tiles as fft_tab_kernel.
+template <int N, int XB, int SIGN>
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+    fft_tab_tma_kernel(FftArgs a) {
+  extern __shared__ __align__(1024) double2 smem[];
+  constexpr int TPR = N / 16, SIZE = RowLayout<N, XB>::SIZE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + XB * SIZE);
+  const int tid = threadIdx.x;
+  const int xl = tid % XB, t = tid / XB;
+  const int y = blockIdx.y;
+  if (y == a.skip_y) return;
+  const long long f = blockIdx.z;
+  double2* row = smem + xl * SIZE;
+  const bool rows_in = a.tab_out != nullptr;
+  int rtab[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int p = t + e * TPR;
+    rtab[e] = rows_in ? __ldg(&a.tab_out[(long long)y * N + p])
+                      : (p != a.zero_p ? __ldg(&a.tab_in[(long long)y * N + p]) : -1);
+  }
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t phase = 0;
+  for (int xt = blockIdx.x; xt * XB < a.X; xt += gridDim.x) {
+    const int x = xt * XB + xl;
+    double2 v[16];
+    if (rows_in) {
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic use of the rows
+        mbar_expect_tx(bar, XB * N * sizeof(double2));
+        const double2* r0 = a.src + f * a.fs_in + (long long)y * a.sy_in + (long long)xt * XB * a.sx_in;
+#pragma unroll
+        for (int r = 0; r < XB; ++r)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_addr(smem + r * SIZE)),
+                       "l"(r0 + r * a.sx_in), "r"((uint32_t)(N * sizeof(double2))), "r"(smem_addr(bar))
+                       : "memory");
+      }
+      while (!mbar_try_wait(bar, phase)) {
+      }
+      phase ^= 1;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int p = t + e * TPR;
+        v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : row[p];
+      }
+      __syncthreads();   // the rows are in registers before the exchange reuses them
+    } else {
+      const double2* base = a.src + f * a.fs_in + x;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = rtab[e] >= 0 ? base[(long long)rtab[e] * a.tabJ] : make_double2(0.0, 0.0);
+    }
+    fft_rows<N, SIGN>(v, t, a.tw, row);   // ends behind a barrier: the exchange rows are free
+    const double wx = a.weight ? __ldg(&a.w[a.jbase + x]) : 1.0;
+    if (rows_in) {
+      double2* tbase = a.dst + f * a.fs_out + x;
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (rtab[e] >= 0) tbase[(long long)rtab[e] * a.tabJ] = make_double2(v[e].x * wx, v[e].y * wx);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) row[t + e * TPR] = make_double2(v[e].x * wx, v[e].y * wx);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        double2* d0 = a.dst + f * a.fs_out + (long long)y * a.sy_out + (long long)xt * XB * a.sx_out;
+#pragma unroll
+        for (int r = 0; r < XB; ++r)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d0 + r * a.sx_out),
+                       "r"(smem_addr(smem + r * SIZE)), "r"((uint32_t)(N * sizeof(double2)))
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncthreads();   // the rows have been read before the next tile's exchange writes them
+    }
+  }
+}
+
 }  // namespace so3

@@ -172,7 +172,8 @@ struct so3_plan_s {
 
 namespace {
 
-int g_fft_tab_loop = 8;   // dev knob fft_tab_loop: x-tiles per CTA of the row-table passes (0: per-tile kernel)
+int g_fft_tab_loop = 8;
+int g_fft_tab_tma = 1;     // dev knob fft_tab_tma: row-table passes move their plain side by bulk copies   // dev knob fft_tab_loop: x-tiles per CTA of the row-table passes (0: per-tile kernel)
 
 template <int N, int XB>
 int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
@@ -180,6 +181,17 @@ int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st)
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
   dim3 grid((a.X + XB - 1) / XB, a.Y, batch);
   const bool tab = a.tab_in || a.tab_out;
+  if (tab && g_fft_tab_loop > 0 && g_fft_tab_tma && XB == 4 && (N == 256 || N == 512 || N == 1024) && a.X % XB == 0 &&
+      !(a.tab_in && a.tab_out) && (a.tab_out ? a.sp_in == 1 : a.sp_out == 1)) {
+    constexpr int NT = (N == 256 || N == 512 || N == 1024) ? N : 256;
+    auto kt = sign > 0 ? so3::fft_tab_tma_kernel<NT, 4, +1> : so3::fft_tab_tma_kernel<NT, 4, -1>;
+    const size_t smem_t = (size_t)4 * so3::RowLayout<NT, 4>::SIZE * sizeof(double2) + 16;
+    if (smem_t > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
+    grid.x = (grid.x + g_fft_tab_loop - 1) / g_fft_tab_loop;
+    kt<<<grid, threads, smem_t, st>>>(a);
+    SO3_CUDA(cudaGetLastError());
+    return SO3_OK;
+  }
   if (tab && g_fft_tab_loop > 0) {
     auto kt = sign > 0 ? so3::fft_tab_kernel<N, XB, +1> : so3::fft_tab_kernel<N, XB, -1>;
     if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -930,6 +942,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
   if (k == "fft_tma") { p->fft_tma = value; return SO3_OK; }
   if (k == "fft_tab_loop") { g_fft_tab_loop = value; return SO3_OK; }
+  if (k == "fft_tab_tma") { g_fft_tab_tma = value; return SO3_OK; }
   if (k == "fft_bulkin") { g_fft_bulkin = value; return SO3_OK; }
   if (k == "fft_bulkout") { g_fft_bulkout = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
