@@ -162,7 +162,7 @@ __device__ __forceinline__ void tensor_store5(const CUtensorMap* map, int c0, in
 // (2 XB doubles, p mod 256, p / 256, 1, 1).  The per-thread 64-byte chunk stores filled the
 // LSU queue (lg_throttle 12.7 % of the plain pass's stalls).
 template <int N, int XB, int SIGN, bool BULKIN = false>
-__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 64 ? 3 : XB * N / 16 <= 128 ? 4 : XB * N / 16 <= 256 ? 2 : 1))
     fft_pass_tstore_kernel(const __grid_constant__ CUtensorMap omap, FftArgs a) {
   extern __shared__ __align__(1024) double2 smem[];
   constexpr int TPR = N / 16, SIZE = RowLayout<N, XB>::SIZE;
@@ -224,7 +224,11 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
 // Chunks-in pass (K4a, K4b) as fft_pass_kernel, with the tile's chunk side arriving by ONE
 // tensor load into the exchange rows (mbarrier after the rows) instead of 16 per-thread loads.
 template <int N, int XB, int SIGN, bool BULKOUT = false>
-__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N / 16 <= 256 ? 2 : 1))
+// CTAs per SM: 3 at 2B = 1024 (85 registers, a few spilled) and 4 at 2B = 512: the CTAs mostly
+// wait on their tile's tensor load (ncu: half the stall samples on the mbarrier poll), and more
+// resident CTAs hide more of it (B=512 inverse stage 12.5 -> 11.1 ms, B=256 1.53 -> 1.31 ms; the
+// rows-in kernel is faster at two CTAs at 2B = 1024, 11.75 vs 12.7 ms, and at four at 2B = 512).
+__global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 64 ? 3 : XB * N / 16 <= 128 ? 4 : XB * N / 16 <= 256 ? 3 : 1))
     fft_pass_tload_kernel(const __grid_constant__ CUtensorMap imap, FftArgs a) {
   extern __shared__ __align__(1024) double2 smem[];
   constexpr int TPR = N / 16;
