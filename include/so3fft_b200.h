@@ -137,9 +137,10 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * plans with 2B <= 64, 0 = per-function kernels), "fft_fused" (1 = one-pass 2-D slice FFT for
  * 2B <= 64, 0 = two passes), "fft_tma" (1 = FFT tiles move their strided side by TMA tensor
  * copies: passes at 2B in {256, 512, 1024} and the one-pass slices; 0 = per-thread loads and
- * stores; bit-identical), "fft_tab_loop" (x-tiles per CTA of the
- * sharded row-table FFT passes, 0 = one tile per CTA; process-wide).  Unknown names fail with
- * SO3_ERR_INVALID. */
+ * stores; bit-identical), "fft_bulkin" / "fft_bulkout" (the TMA passes' row side by 1-D bulk
+ * copies: 1 / 0, -1 = automatic), "fft_tab_loop" (x-tiles per CTA of the sharded row-table FFT
+ * passes, 0 = one tile per CTA), "fft_tab_tma" (row-table passes' plain side by bulk copies).
+ * All knobs are per plan.  Unknown names fail with SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */

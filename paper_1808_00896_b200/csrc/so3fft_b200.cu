@@ -165,6 +165,10 @@ struct so3_plan_s {
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
   int fft_tma = 1;    // TMA-fed FFT kernels (fft_tma.cuh): passes at 2B in {256, 512, 1024}, one-pass slices
+  int fft_bulkin = 1;    // rows-in TMA passes also load their rows by 1-D bulk copies
+  int fft_bulkout = -1;  // chunks-in TMA passes store their rows by 1-D bulk copies (-1: 2B >= 512)
+  int fft_tab_loop = 8;  // x-tiles per CTA of the sharded row-table passes (0: one tile per CTA)
+  int fft_tab_tma = 1;   // row-table passes move their plain-strided side by bulk copies
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
 };
 
@@ -172,30 +176,28 @@ struct so3_plan_s {
 
 namespace {
 
-int g_fft_tab_loop = 8;
-int g_fft_tab_tma = 1;     // dev knob fft_tab_tma: row-table passes move their plain side by bulk copies   // dev knob fft_tab_loop: x-tiles per CTA of the row-table passes (0: per-tile kernel)
 
 template <int N, int XB>
-int launch_fft_pow2(const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
+int launch_fft_pow2(const so3_plan_s* p, const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
   const int threads = XB * N / 16;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2);
   dim3 grid((a.X + XB - 1) / XB, a.Y, batch);
   const bool tab = a.tab_in || a.tab_out;
-  if (tab && g_fft_tab_loop > 0 && g_fft_tab_tma && XB == 4 && (N == 256 || N == 512 || N == 1024) && a.X % XB == 0 &&
+  if (tab && p->fft_tab_loop > 0 && p->fft_tab_tma && XB == 4 && (N == 256 || N == 512 || N == 1024) && a.X % XB == 0 &&
       !(a.tab_in && a.tab_out) && (a.tab_out ? a.sp_in == 1 : a.sp_out == 1)) {
     constexpr int NT = (N == 256 || N == 512 || N == 1024) ? N : 256;
     auto kt = sign > 0 ? so3::fft_tab_tma_kernel<NT, 4, +1> : so3::fft_tab_tma_kernel<NT, 4, -1>;
     const size_t smem_t = (size_t)4 * so3::RowLayout<NT, 4>::SIZE * sizeof(double2) + 16;
     if (smem_t > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
-    grid.x = (grid.x + g_fft_tab_loop - 1) / g_fft_tab_loop;
+    grid.x = (grid.x + p->fft_tab_loop - 1) / p->fft_tab_loop;
     kt<<<grid, threads, smem_t, st>>>(a);
     SO3_CUDA(cudaGetLastError());
     return SO3_OK;
   }
-  if (tab && g_fft_tab_loop > 0) {
+  if (tab && p->fft_tab_loop > 0) {
     auto kt = sign > 0 ? so3::fft_tab_kernel<N, XB, +1> : so3::fft_tab_kernel<N, XB, -1>;
     if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    grid.x = (grid.x + g_fft_tab_loop - 1) / g_fft_tab_loop;
+    grid.x = (grid.x + p->fft_tab_loop - 1) / p->fft_tab_loop;
     kt<<<grid, threads, smem, st>>>(a);
     SO3_CUDA(cudaGetLastError());
     return SO3_OK;
@@ -239,8 +241,6 @@ EncodeTiledFn encode_tiled() {
 
 // TMA-fed pass (fft_tma.cuh): RI passes read rows / write chunks, CI passes the reverse.  The
 // chunk side is described by a 5-D tensor map over (x as doubles, p mod 256, p / 256, y, f).
-int g_fft_bulkout = -1; // dev knob fft_bulkout: chunks-in passes store their rows by 1-D bulk copies (-1: 2B >= 512)
-int g_fft_bulkin = 1;   // dev knob fft_bulkin: rows-in passes also load their rows by 1-D bulk copies
 
 template <int N, int SIGN>
 auto sign_kernel_tstore() { return so3::fft_pass_tstore_kernel<N, 4, SIGN>; }
@@ -250,25 +250,26 @@ int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStr
 
 // XB (rows per CTA) = the chunk width on the transposed side (XB * 16 bytes).
 template <int N>
-int launch_fft_xb(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int xb) {
+int launch_fft_xb(const so3_plan_s* p, const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int xb) {
   switch (xb) {
-    case 2: return launch_fft_pow2<N, 2>(a, sign, batch, st);
-    case 4: return launch_fft_pow2<N, 4>(a, sign, batch, st);
-    case 8: return launch_fft_pow2<N, 8>(a, sign, batch, st);
-    default: return launch_fft_pow2<N, 16>(a, sign, batch, st);
+    case 2: return launch_fft_pow2<N, 2>(p, a, sign, batch, st);
+    case 4: return launch_fft_pow2<N, 4>(p, a, sign, batch, st);
+    case 8: return launch_fft_pow2<N, 8>(p, a, sign, batch, st);
+    default: return launch_fft_pow2<N, 16>(p, a, sign, batch, st);
   }
 }
 
-int launch_fft(const so3::FftArgs& a, int sign, int batch, cudaStream_t st, int xb_override = 0) {
+int launch_fft(const so3_plan_s* p, const so3::FftArgs& a, int sign, int batch, cudaStream_t st) {
+  const int xb_override = p->fft_wide;
   switch (a.n) {
-    case 16: return launch_fft_pow2<16, 16>(a, sign, batch, st);
-    case 32: return launch_fft_pow2<32, 32>(a, sign, batch, st);
-    case 64: return launch_fft_pow2<64, 32>(a, sign, batch, st);
-    case 128: return launch_fft_pow2<128, 32>(a, sign, batch, st);
-    case 256: return launch_fft_xb<256>(a, sign, batch, st, xb_override ? xb_override : 4);
-    case 512: return launch_fft_xb<512>(a, sign, batch, st, xb_override ? xb_override : 4);
-    case 1024: return launch_fft_xb<1024>(a, sign, batch, st, xb_override ? xb_override : 4);
-    case 2048: return launch_fft_pow2<2048, 2>(a, sign, batch, st);
+    case 16: return launch_fft_pow2<16, 16>(p, a, sign, batch, st);
+    case 32: return launch_fft_pow2<32, 32>(p, a, sign, batch, st);
+    case 64: return launch_fft_pow2<64, 32>(p, a, sign, batch, st);
+    case 128: return launch_fft_pow2<128, 32>(p, a, sign, batch, st);
+    case 256: return launch_fft_xb<256>(p, a, sign, batch, st, xb_override ? xb_override : 4);
+    case 512: return launch_fft_xb<512>(p, a, sign, batch, st, xb_override ? xb_override : 4);
+    case 1024: return launch_fft_xb<1024>(p, a, sign, batch, st, xb_override ? xb_override : 4);
+    case 2048: return launch_fft_pow2<2048, 2>(p, a, sign, batch, st);
     default: return launch_fft_direct(a, sign, batch, st);
   }
 }
@@ -330,7 +331,7 @@ int launch_fft2d(const so3_plan_s* p, int sign, const void* src, void* dst, cuda
 
 // Rows-in pass with a TMA tensor store of each tile's chunk side (fft_tma.cuh).
 template <int N, int SIGN>
-int launch_fft_tstore_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
+int launch_fft_tstore_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, cudaStream_t st) {
   constexpr int XB = 4;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return -1;
@@ -345,7 +346,7 @@ int launch_fft_tstore_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
-  auto k = g_fft_bulkin ? (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1, true> : so3::fft_pass_tstore_kernel<N, XB, -1, true>)
+  auto k = p->fft_bulkin ? (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1, true> : so3::fft_pass_tstore_kernel<N, XB, -1, true>)
                         : sign_kernel_tstore<N, SIGN>();
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
@@ -355,7 +356,7 @@ int launch_fft_tstore_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
 
 // Chunks-in pass with a TMA tensor load of each tile's chunk side (fft_tma.cuh).
 template <int N, int SIGN>
-int launch_fft_tload_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
+int launch_fft_tload_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, cudaStream_t st) {
   constexpr int XB = 4;
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return -1;
@@ -371,7 +372,7 @@ int launch_fft_tload_t(const so3::FftArgs& a, int batch, cudaStream_t st) {
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
-  const bool bulkout = g_fft_bulkout < 0 ? N >= 512 : g_fft_bulkout != 0;
+  const bool bulkout = p->fft_bulkout < 0 ? N >= 512 : p->fft_bulkout != 0;
   auto k = bulkout ? (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1, true> : so3::fft_pass_tload_kernel<N, XB, -1, true>)
                          : (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1> : so3::fft_pass_tload_kernel<N, XB, -1>);
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -386,16 +387,16 @@ int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStr
   if (a.n != 256 && a.n != 512 && a.n != 1024) return -1;
   if (a.sp_in == 1 && a.sx_out == 1) {
     switch (a.n) {
-      case 256: return sign > 0 ? launch_fft_tstore_t<256, +1>(a, p->batch, st) : launch_fft_tstore_t<256, -1>(a, p->batch, st);
-      case 512: return sign > 0 ? launch_fft_tstore_t<512, +1>(a, p->batch, st) : launch_fft_tstore_t<512, -1>(a, p->batch, st);
-      default: return sign > 0 ? launch_fft_tstore_t<1024, +1>(a, p->batch, st) : launch_fft_tstore_t<1024, -1>(a, p->batch, st);
+      case 256: return sign > 0 ? launch_fft_tstore_t<256, +1>(p, a, p->batch, st) : launch_fft_tstore_t<256, -1>(p, a, p->batch, st);
+      case 512: return sign > 0 ? launch_fft_tstore_t<512, +1>(p, a, p->batch, st) : launch_fft_tstore_t<512, -1>(p, a, p->batch, st);
+      default: return sign > 0 ? launch_fft_tstore_t<1024, +1>(p, a, p->batch, st) : launch_fft_tstore_t<1024, -1>(p, a, p->batch, st);
     }
   }
   if (a.sp_in != 1 && a.sx_in == 1 && a.sp_out == 1 && !a.weight) {
     switch (a.n) {
-      case 256: return sign > 0 ? launch_fft_tload_t<256, +1>(a, p->batch, st) : launch_fft_tload_t<256, -1>(a, p->batch, st);
-      case 512: return sign > 0 ? launch_fft_tload_t<512, +1>(a, p->batch, st) : launch_fft_tload_t<512, -1>(a, p->batch, st);
-      default: return sign > 0 ? launch_fft_tload_t<1024, +1>(a, p->batch, st) : launch_fft_tload_t<1024, -1>(a, p->batch, st);
+      case 256: return sign > 0 ? launch_fft_tload_t<256, +1>(p, a, p->batch, st) : launch_fft_tload_t<256, -1>(p, a, p->batch, st);
+      case 512: return sign > 0 ? launch_fft_tload_t<512, +1>(p, a, p->batch, st) : launch_fft_tload_t<512, -1>(p, a, p->batch, st);
+      default: return sign > 0 ? launch_fft_tload_t<1024, +1>(p, a, p->batch, st) : launch_fft_tload_t<1024, -1>(p, a, p->batch, st);
     }
   }
   return -1;
@@ -941,10 +942,10 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
   if (k == "fft_tma") { p->fft_tma = value; return SO3_OK; }
-  if (k == "fft_tab_loop") { g_fft_tab_loop = value; return SO3_OK; }
-  if (k == "fft_tab_tma") { g_fft_tab_tma = value; return SO3_OK; }
-  if (k == "fft_bulkin") { g_fft_bulkin = value; return SO3_OK; }
-  if (k == "fft_bulkout") { g_fft_bulkout = value; return SO3_OK; }
+  if (k == "fft_tab_loop") { p->fft_tab_loop = value; return SO3_OK; }
+  if (k == "fft_tab_tma") { p->fft_tab_tma = value; return SO3_OK; }
+  if (k == "fft_bulkin") { p->fft_bulkin = value; return SO3_OK; }
+  if (k == "fft_bulkout") { p->fft_bulkout = value; return SO3_OK; }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
@@ -969,7 +970,7 @@ int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* st
   for (int pass = 0; pass < 2; ++pass) {
     const so3::FftArgs a = pass == 0 ? fft_pass_args(p, 0, samples, p->d_scratch) : fft_pass_args(p, 1, p->d_scratch, spectrum);
     int rc = launch_fft_tma(p, a, +1, st);
-    if (rc < 0) rc = launch_fft(a, +1, p->batch, st, p->fft_wide);
+    if (rc < 0) rc = launch_fft(p, a, +1, p->batch, st);
     if (rc) return rc;
   }
   return SO3_OK;
@@ -984,7 +985,7 @@ int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream)
   for (int pass = 2; pass < 4; ++pass) {
     const so3::FftArgs a = pass == 2 ? fft_pass_args(p, 2, spectrum, p->d_scratch) : fft_pass_args(p, 3, p->d_scratch, samples);
     int rc = launch_fft_tma(p, a, -1, st);
-    if (rc < 0) rc = launch_fft(a, -1, p->batch, st, p->fft_wide);
+    if (rc < 0) rc = launch_fft(p, a, -1, p->batch, st);
     if (rc) return rc;
   }
   return SO3_OK;
@@ -1067,9 +1068,9 @@ int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* str
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const so3::FftArgs a0 = shard_pass_args(p, 0, slab, p->d_scratch);   // plain strides: TMA-fed when it applies
   int rc = launch_fft_tma(p, a0, +1, st);
-  if (rc < 0) rc = launch_fft(a0, +1, 1, st, p->fft_wide);
+  if (rc < 0) rc = launch_fft(p, a0, +1, 1, st);
   if (rc) return rc;
-  return launch_fft(shard_pass_args(p, 1, p->d_scratch, send), +1, 1, st, p->fft_wide);
+  return launch_fft(p, shard_pass_args(p, 1, p->d_scratch, send), +1, 1, st);
 }
 
 #define CHECK_CHUNK(p, q) \
@@ -1109,11 +1110,11 @@ int so3_shard_dwt_synthesis(so3_plan_t p, const void* coeffs, void* send, void* 
 int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(recv); CHECK_PTR(slab);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = launch_fft(shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st, p->fft_wide);
+  int rc = launch_fft(p, shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st);
   if (rc) return rc;
   const so3::FftArgs a3 = shard_pass_args(p, 3, p->d_scratch, slab);   // plain strides: TMA-fed when it applies
   rc = launch_fft_tma(p, a3, -1, st);
-  return rc >= 0 ? rc : launch_fft(a3, -1, 1, st, p->fft_wide);
+  return rc >= 0 ? rc : launch_fft(p, a3, -1, 1, st);
 }
 
 // Direct O(B^6) transforms (soft.py:212-256): closed-form Wigner functions, no plan.
