@@ -162,6 +162,10 @@ struct so3_plan_s {
   std::vector<int64_t> chunk_off;       // prefix of chunk_pairs
   int dwt_variant = SO3_DWT_MMA;
   int syn_jw = 0;     // dev knob (SO3_SYN_JW): beta indices per warp in the synthesis kernel
+  int ana_split = 1;  // 2B = 1024 analysis: each cluster over two 4-warp CTAs (dwt_mma.cuh, SPLIT = 2)
+  long long rc_entries = 0;       // recurrence-table entries = sum over the plan's clusters of (B - m)
+  double2* d_pbuf = nullptr;      // split analysis: per-half partial sums, 2 x rc_entries x 8
+  unsigned* d_pcnt = nullptr;     // split analysis: per-cluster arrival counters
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
   int fft_tma = 1;    // TMA-fed FFT kernels (fft_tma.cuh): passes at 2B in {256, 512, 1024}, one-pass slices
@@ -553,6 +557,33 @@ int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, 
   return SO3_OK;
 }
 
+// 2B = 1024 analysis with each cluster over two 4-warp CTAs; the partial-sum scratch and the
+// counters are allocated on first use (2 x 2.86 GB at B = 512).
+int launch_dwt_ana_split(const so3_plan_s* pc, so3::DwtArgs a, unsigned ncl, cudaStream_t st) {
+  so3_plan_s* p = const_cast<so3_plan_s*>(pc);
+  if (!p->d_pbuf) {
+    const size_t pb = (size_t)2 * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2);
+    cudaError_t e = cudaMalloc((void**)&p->d_pbuf, pb);
+    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("split-analysis scratch: ") + cudaGetErrorString(e));
+    e = cudaMalloc((void**)&p->d_pcnt, (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned));
+    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("split-analysis counters: ") + cudaGetErrorString(e));
+    e = cudaMemset(p->d_pcnt, 0, (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned));
+    if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("split-analysis counters: ") + cudaGetErrorString(e));
+    p->bytes += (int64_t)pb + p->nclusters * (int64_t)sizeof(unsigned);
+  }
+  a.pbuf = p->d_pbuf;
+  a.pstride = p->rc_entries * 8;
+  a.pcnt = p->d_pcnt;
+  constexpr int JW = 128, W = 4;
+  using SM = so3::MmaSmem<JW>;
+  const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double);
+  auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
+  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 template <bool ANALYSIS>
 int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st,
                int64_t chunk_pairs = -1) {
@@ -578,6 +609,9 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.J = p->sharded ? p->J : p->n;
   // sharded: spec is one chunk [h][pairs_chunk][J] of layout B (chunk_pairs; default = all pairs)
   a.slab_stride = p->sharded ? (long long)(chunk_pairs >= 0 ? chunk_pairs : p->pairs_rank) * p->J : 0;
+  a.pbuf = nullptr;
+  a.pstride = 0;
+  a.pcnt = nullptr;
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
@@ -586,6 +620,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
     if (syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
   }
+  if (ANALYSIS && p->ana_split && p->dwt_variant != SO3_DWT_SIMT && p->n == 1024 && p->batch == 1)
+    return launch_dwt_ana_split(p, a, ncl, st);
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
       case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
@@ -707,6 +743,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
     rc_off[i] = rc_entries;
     rc_entries += b - cl[i].m;   // one (alpha, beta, mu) per degree
   }
+  p->rc_entries = rc_entries;
   rc_entries = std::max(rc_entries, 1LL);
   std::vector<int2> bases(ncl, make_int2(0, 0));
   std::vector<double2> lnorm(ncl, make_double2(0.0, 0.0));
@@ -920,6 +957,8 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_spec);
   cudaFree(p->d_rc);
   cudaFree(p->d_rc_off);
+  cudaFree(p->d_pbuf);
+  cudaFree(p->d_pcnt);
   cudaFree(p->d_row_global);
   cudaFree(p->d_row_local);
   cudaFree(p->d_grid_stage);
@@ -938,6 +977,7 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   const std::string k(name);
   if (k == "dwt_variant") return so3_plan_set_dwt_variant(p, value);
   if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
+  if (k == "ana_split") { p->ana_split = value; return SO3_OK; }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }
