@@ -574,7 +574,8 @@ int launch_dwt_ana_split(const so3_plan_s* pc, so3::DwtArgs a, unsigned ncl, cud
   a.pbuf = p->d_pbuf;
   a.pstride = p->rc_entries * 8;
   a.pcnt = p->d_pcnt;
-  constexpr int JW = 128, W = 4;
+  constexpr int JW = 128;
+  const int W = p->n / JW / 2;   // warps per half
   using SM = so3::MmaSmem<JW>;
   const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
@@ -620,7 +621,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
     if (syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
   }
-  if (ANALYSIS && p->ana_split && p->dwt_variant != SO3_DWT_SIMT && p->n == 1024 && p->batch == 1)
+  if (ANALYSIS && p->ana_split && p->dwt_variant != SO3_DWT_SIMT && (p->n == 1024 || (p->n == 512 && p->ana_split > 1)) &&
+      p->batch == 1)
     return launch_dwt_ana_split(p, a, ncl, st);
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
