@@ -616,7 +616,7 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
-  const int syn_jw = p->syn_jw ? p->syn_jw : (p->n == 512 ? 64 : 0);
+  const int syn_jw = p->syn_jw ? p->syn_jw : (p->n >= 512 ? 64 : 0);   // 16 warps per SM (B=512: 32.8 vs 33.7 ms with JW = 128)
   if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && syn_jw && (p->n + syn_jw - 1) / syn_jw <= 16) {
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
     if (syn_jw == 32) return launch_dwt_mma<32>(false, a, p->n, ncl, p->batch, st);
