@@ -530,3 +530,24 @@ def test_wigner_recurrence_at_b512_against_50_digit_values(golden):
     ref_err = np.abs(g["ref_fp64"] - g["value"])
     assert err.max() <= max(ref_err.max(), 1e-13), (err.max(), ref_err.max())
     assert err.max() < 5e-12
+
+
+def test_split_analysis_matches_one_cta_reduction_b512():
+    """2B = 1024: the analysis over two CTAs per cluster (partials combined in a fixed order by
+    the CTA that finishes second) agrees with the one-CTA reduction to rounding, and repeated
+    launches are bit-identical (the per-cluster counters re-arm themselves)."""
+    b = 512
+    n = 2 * b
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    spec = torch.randn(n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
+    plan = plan_for(b)
+    C = so3.coeff_count(b)
+    outs = []
+    for split in (0, 1, 1):
+        plan.set_knob("ana_split", split)
+        o = torch.zeros(C, dtype=torch.complex128, device="cuda")
+        so3.dwt_analysis(plan, spec, o)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert (outs[1] - outs[0]).abs().max().item() <= 1e-14 * outs[0].abs().max().item()
+    assert torch.equal(outs[1], outs[2])
