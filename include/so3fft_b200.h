@@ -140,7 +140,9 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * stores; bit-identical), "fft_bulkin" / "fft_bulkout" (the TMA passes' row side by 1-D bulk
  * copies: 1 / 0, -1 = automatic), "fft_tab_loop" (x-tiles per CTA of the sharded row-table FFT
  * passes, 0 = one tile per CTA), "fft_tab_tma" (row-table passes' plain side by bulk copies).
- * All knobs are per plan.  Unknown names fail with SO3_ERR_INVALID. */
+ * "ana_split" (2B = 1024 analysis over two CTAs per cluster: 1 = on (default), 0 = one CTA;
+ * same results to rounding, deterministic).  All knobs are per plan.  Unknown names fail with
+ * SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */
