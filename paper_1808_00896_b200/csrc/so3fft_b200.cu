@@ -515,7 +515,7 @@ int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cu
   const size_t smem = ((size_t)warps * 8 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, FG>;
   SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a);
+  k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a, so3::SplitArgs{nullptr, 0, nullptr});
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
@@ -571,16 +571,14 @@ int launch_dwt_ana_split(const so3_plan_s* pc, so3::DwtArgs a, unsigned ncl, cud
     if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("split-analysis counters: ") + cudaGetErrorString(e));
     p->bytes += (int64_t)pb + p->nclusters * (int64_t)sizeof(unsigned);
   }
-  a.pbuf = p->d_pbuf;
-  a.pstride = p->rc_entries * 8;
-  a.pcnt = p->d_pcnt;
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
   constexpr int JW = 128;
   const int W = p->n / JW / 2;   // warps per half
   using SM = so3::MmaSmem<JW>;
   const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
   SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a);
+  k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a, sp);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
@@ -610,9 +608,6 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.J = p->sharded ? p->J : p->n;
   // sharded: spec is one chunk [h][pairs_chunk][J] of layout B (chunk_pairs; default = all pairs)
   a.slab_stride = p->sharded ? (long long)(chunk_pairs >= 0 ? chunk_pairs : p->pairs_rank) * p->J : 0;
-  a.pbuf = nullptr;
-  a.pstride = 0;
-  a.pcnt = nullptr;
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
