@@ -122,6 +122,39 @@ def test_sampled_oracle_at_b256():
             assert rel_of_max(mine, col) < 1e-12, (m, mp)
 
 
+def test_sampled_oracle_at_b512():
+    """B=512 (2B = 1024: TMA-fed FFT passes, split analysis): FFT stage on sampled beta slices and
+    DWT on sampled clusters (origin, axis, diagonal, interior, the last degrees) vs the oracle,
+    fed the same inputs; the grid stays on the GPU and only the sampled slices / rows come back."""
+    b, n = 512, 1024
+    plan = plan_for(b)
+    gen = torch.Generator(device="cuda").manual_seed(512)
+    gd = torch.randn(n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
+    spec = torch.empty_like(gd)
+    so3.fft_analysis(plan, gd, spec)
+    cube = gd.view(n, n, n)
+    sv = spec.view(n, n, n)                          # stored [m'][m][j]
+    w = O.beta_weights(b)
+    for j in (0, 301, 1023):
+        ref = O.slice_dft(cube[:, j, :].cpu().numpy(), +1) * w[j]
+        got = sv[:, :, j].cpu().numpy().T.copy()    # -> [m][m']
+        got[:, b] = ref[:, b]                        # column m' = B is never written (not needed)
+        assert rel_of_max(got, ref) < 1e-12          # 1024^2-point 2-D DFT: ~3e-13 measured
+    del cube
+    coeffs = torch.empty(O.n_coeffs(b), dtype=torch.complex128, device="cuda")
+    so3.dwt_analysis(plan, spec, coeffs)
+    got = coeffs.cpu().numpy()
+    betas = O.beta_nodes(b)
+    v = (2.0 * np.arange(b) + 1.0) / (8.0 * math.pi * b)
+    for (bm, bmp) in [(0, 0), (7, 0), (300, 300), (400, 123), (511, 510)]:
+        rows = O.recurrence_rows(bm, bmp, betas, b)
+        for (m, mp, tag) in O.cluster_members(bm, bmp):
+            srow = sv[mp % n, m % n, :].cpu().numpy()
+            col = O.analysis_column(O.member_matrix(rows, tag, bm, bmp, b), v[bm:], np.ones(n), srow)
+            mine = got[O.pair_slots(m, mp, b)]
+            assert rel_of_max(mine, col) < 1e-12, (m, mp)
+
+
 # ---------------------------------------------------------------- stages and Wigner rows
 
 def test_wigner_rows_match_reference_golden(golden):
