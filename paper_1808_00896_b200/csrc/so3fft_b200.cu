@@ -230,24 +230,16 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 EncodeTiledFn encode_tiled() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static const EncodeTiledFn fn = [] {   // thread-safe one-time query
     void* ptr = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(ptr);
-  }
+      return reinterpret_cast<EncodeTiledFn>(ptr);
+    return static_cast<EncodeTiledFn>(nullptr);
+  }();
   return fn;
 }
-
-// TMA-fed pass (fft_tma.cuh): RI passes read rows / write chunks, CI passes the reverse.  The
-// chunk side is described by a 5-D tensor map over (x as doubles, p mod 256, p / 256, y, f).
-
-template <int N, int SIGN>
-auto sign_kernel_tstore() { return so3::fft_pass_tstore_kernel<N, 4, SIGN>; }
 
 // returns -1 when the TMA pass does not apply (row tables, odd sizes, knob off)
 int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st);
@@ -277,8 +269,6 @@ int launch_fft(const so3_plan_s* p, const so3::FftArgs& a, int sign, int batch, 
     default: return launch_fft_direct(a, sign, batch, st);
   }
 }
-
-EncodeTiledFn encode_tiled();
 
 // Slice transform with the pair-major side by TMA (fft_tma.cuh): tensor map over X with dims
 // (j as doubles, m', m, f) -- strides n^2, n, n^3 complex128 -- and box (2, N, N, 1).
@@ -351,7 +341,7 @@ int launch_fft_tstore_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, c
     return -1;
   const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
   auto k = p->fft_bulkin ? (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1, true> : so3::fft_pass_tstore_kernel<N, XB, -1, true>)
-                        : sign_kernel_tstore<N, SIGN>();
+                        : (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1> : so3::fft_pass_tstore_kernel<N, XB, -1>);
   if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
   SO3_CUDA(cudaGetLastError());
