@@ -623,6 +623,35 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-exec this command as N ranks (one
+    process per GPU) through torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def launch_check(rank: int, world: int) -> None:
+    """--launch-check: gloo rendezvous of all ranks (no GPU work); rank 0 prints who reported."""
+    import torch
+    import torch.distributed as tdist
+    tdist.init_process_group("gloo")
+    seen = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    tdist.all_gather(seen, torch.tensor([rank], dtype=torch.int64))
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": world, "ranks": [int(t.item()) for t in seen],
+                          "backend": tdist.get_backend()}), flush=True)
+    tdist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -641,12 +670,22 @@ def main() -> None:
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-slices", type=int, default=64)
     ap.add_argument("--cpu-clusters", type=int, default=2048)
+    ap.add_argument("--launch-check", action="store_true",
+                    help="rendezvous only (gloo): every rank reports in, rank 0 prints the ranks it saw")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules require >= 3 warm-up steps", file=sys.stderr)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+                 f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus")
+    if args.launch_check:
+        launch_check(rank, world)
+        return
     dist = None
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
@@ -656,6 +695,10 @@ def main() -> None:
     if world > 1 or (mode == "sharded" and "MASTER_ADDR" in os.environ):
         import torch
         import torch.distributed as tdist
+        # communicator init lines (ranks, nRanks, NVLS/P2P transport) on stderr, so the driver can
+        # see N ranks while stdout keeps the one JSON line
+        for k, v in (("NCCL_DEBUG", "INFO"), ("NCCL_DEBUG_SUBSYS", "INIT"), ("NCCL_DEBUG_FILE", "/dev/stderr")):
+            os.environ.setdefault(k, v)
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
         tdist.init_process_group("nccl")
         dist = tdist

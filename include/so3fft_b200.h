@@ -21,6 +21,16 @@
  * Errors: every function returns SO3_OK (0) or a nonzero status; the message of
  * the last failure on the calling thread is so3_last_error().  SO3_ERR_INVALID
  * corresponds to the reference's ValueError (bad bandwidth, size or argument).
+ *
+ * Plans and concurrency: a plan is read-only tables PLUS per-plan scratch (the FFT
+ * intermediate, the pair-major spectrum, the split-analysis partial sums and counters,
+ * the host-path staging buffers).  Every transform on one plan uses that scratch, so calls
+ * on ONE plan must be stream-ordered: issue them on one stream, or order the streams
+ * yourself (events).  Different plans are independent and may run concurrently on any
+ * streams or threads.  (The reference TransformPlan is immutable and may be shared; give
+ * each concurrent stream its own plan here.)  No call allocates device memory except
+ * so3_plan_create*, so3_plan_set_knob("ana_split") and the first call of a *_host entry
+ * point, so the device entry points can be captured into a CUDA graph.
  */
 #ifndef SO3FFT_B200_H
 #define SO3FFT_B200_H
@@ -74,6 +84,8 @@ int so3_cluster_schedule(int bandwidth, int32_t* bases_host, int32_t* members_ho
 /* ---- plans ---------------------------------------------------------------- */
 
 /* make_plan (soft.py:80-108) for `batch` functions on the current CUDA device.
+ * 1 <= bandwidth <= 512 (SO3_ERR_INVALID otherwise: the DWT kernels hold at most
+ * 2B = 1024 beta indices per cluster, and B = 1024 would need 3 x 137 GB of grids).
  * Builds the beta tables, quadrature weights, twiddles and the cluster schedule
  * on the host (long double), uploads them and allocates the plan's scratch
  * spectrum ((2B)^3 * batch complex128).  matrix_policy / partitioner of the
@@ -106,7 +118,8 @@ int so3_ifsoft_host(so3_plan_t plan, const void* coeffs_host, void* samples_host
 
 /* Forward torus stage: for every beta slice the sign +1 2-D DFT
  * (fft.py:72-76 via soft.py:130-132) times the quadrature weight w_j, written
- * pair-major: spectrum_dev[f][m' mod 2B][m mod 2B][j] (rows m' = B unwritten).
+ * pair-major: spectrum_dev[f][m' mod 2B][m mod 2B][j].  Entries at the Nyquist bin
+ * (m = B or m' = B) hold unspecified values: the DWT never reads them. 
  * Uses the plan's pass-1 scratch; spectrum_dev must be a different buffer. */
 int so3_fft_analysis(so3_plan_t plan, const void* samples_dev, void* spectrum_dev, void* stream);
 
@@ -140,8 +153,10 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * stores; bit-identical), "fft_bulkin" / "fft_bulkout" (the TMA passes' row side by 1-D bulk
  * copies: 1 / 0, -1 = automatic), "fft_tab_loop" (x-tiles per CTA of the sharded row-table FFT
  * passes, 0 = one tile per CTA), "fft_tab_tma" (row-table passes' plain side by bulk copies).
- * "ana_split" (2B = 1024 analysis over two CTAs per cluster: 1 = on (default), 0 = one CTA;
- * same results to rounding, deterministic).  All knobs are per plan.  Unknown names fail with
+ * "ana_split" (analysis of a cluster over two 4-warp CTAs that combine their halves in a
+ * fixed order: 0 = off (one CTA per cluster), 1 = on at 2B = 1024 (default), >= 2 = on at
+ * 2B = 512 and 1024; same results to rounding, deterministic; turning it on allocates the
+ * partial-sum scratch, 2 x 8 x sum_clusters(B - m) complex128).  All knobs are per plan.  Unknown names fail with
  * SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 

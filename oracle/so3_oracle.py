@@ -29,7 +29,8 @@ __all__ = [
     "dft_lastaxis", "slice_dft", "seed_column", "recurrence_rows", "base_pairs",
     "cluster_members", "RELATIONS", "member_matrix", "analysis_column",
     "synthesis_column", "fsoft", "ifsoft", "fsoft_direct", "ifsoft_direct",
-    "closed_form_d", "error_metrics", "degree_of_slot",
+    "closed_form_d", "error_metrics", "degree_of_slot", "fft_analysis_stage", "dwt_analysis_stage",
+    "dwt_synthesis_stage", "fft_synthesis_stage",
 ]
 
 
@@ -288,38 +289,123 @@ def _plan(b: int) -> _Plan:
     return _PLANS[b]
 
 
-def _forward_cluster(args):
-    """One analyze() work item -- soft.py:134-143."""
-    b, bm, bmp, spec_cols = args
+def _forward_block(b: int, bm: int, bmp: int, spectrum: np.ndarray) -> np.ndarray:
+    """One analyze() work item: a stacked (members, B-L) block -- soft.py:134-143."""
     p = _plan(b)
+    n = p.n
     lo = max(bm, bmp)
     rows = recurrence_rows(bm, bmp, p.betas, b)
-    out = []
-    for (m, mp, tag), col in zip(cluster_members(bm, bmp), spec_cols):
-        out.append(analysis_column(member_matrix(rows, tag, bm, bmp, b), p.v[lo:], p.w, col))
-    return out
+    members = cluster_members(bm, bmp)
+    block = np.empty((len(members), b - lo), dtype=np.complex128)
+    for r, (m, mp, tag) in enumerate(members):
+        block[r] = analysis_column(member_matrix(rows, tag, bm, bmp, b), p.v[lo:], p.w, spectrum[m % n, :, mp % n])
+    return block
 
 
-def _inverse_cluster(args):
-    """One synthesize() work item -- soft.py:157-162."""
-    b, bm, bmp, coef_cols = args
+def _inverse_block(b: int, bm: int, bmp: int, flat: np.ndarray) -> np.ndarray:
+    """One synthesize() work item: a stacked (members, 2B) block -- soft.py:157-162."""
     p = _plan(b)
     rows = recurrence_rows(bm, bmp, p.betas, b)
-    return [synthesis_column(member_matrix(rows, tag, bm, bmp, b), c)
-            for (m, mp, tag), c in zip(cluster_members(bm, bmp), coef_cols)]
+    members = cluster_members(bm, bmp)
+    block = np.empty((len(members), p.n), dtype=np.complex128)
+    for r, (m, mp, tag) in enumerate(members):
+        block[r] = synthesis_column(member_matrix(rows, tag, bm, bmp, b), flat[pair_slots(m, mp, b)])
+    return block
 
 
-def _slices_dft(cube: np.ndarray, sign: int, js) -> list[np.ndarray]:
-    return [slice_dft(cube[:, j, :], sign) for j in js]
+# Worker state inherited by the forked pool (schedule.py:189-196, 235-248): only item
+# indices go to the workers and only results come back, as in the reference's run_items.
+_FORK_STATE = None
+
+
+def _one_blas_thread() -> None:
+    """Pool initializer: one BLAS thread per forked worker (the reference's CPU plan pins
+    OMP/OPENBLAS/MKL_NUM_THREADS=1; without it every worker's matvecs oversubscribe the cores)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:  # pragma: no cover - threadpoolctl missing
+        pass
+
+
+def _invoke_item(index: int):
+    worker, items = _FORK_STATE
+    return index, worker(items[index])
 
 
 def _pool_map(fn, items, workers):
+    """run_items (schedule.py:200-257): plain loop for one worker, else a fork pool with
+    dynamic imap_unordered batches of len // (8 workers) items, results put back in order."""
+    global _FORK_STATE
+    items = list(items)
     if workers <= 1 or len(items) <= 1:
         return [fn(it) for it in items]
     import multiprocessing as mp
+    if _FORK_STATE is not None:
+        raise RuntimeError("nested parallel oracle map is not supported")
     chunk = max(1, len(items) // (workers * 8))
-    with mp.get_context("fork").Pool(processes=workers) as pool:
-        return pool.map(fn, items, chunksize=chunk)
+    out = [None] * len(items)
+    _FORK_STATE = (fn, items)
+    try:
+        with mp.get_context("fork").Pool(processes=workers, initializer=_one_blas_thread) as pool:
+            for index, res in pool.imap_unordered(_invoke_item, range(len(items)), chunksize=chunk):
+                out[index] = res
+    finally:
+        _FORK_STATE = None
+    return out
+
+
+def fft_analysis_stage(grid: np.ndarray, b: int, workers: int = 1) -> np.ndarray:
+    """Per-slice sign +1 DFTs into the [m bin, j, m' bin] spectrum -- soft.py:127-132."""
+    n = 2 * b
+    cube = np.asarray(grid, dtype=np.complex128).reshape(n, n, n)
+    spectrum = np.empty((n, n, n), dtype=np.complex128)
+    planes = _pool_map(lambda j: slice_dft(cube[:, j, :], +1), range(n), workers)
+    for j, plane in enumerate(planes):
+        spectrum[:, j, :] = plane
+    return spectrum
+
+
+def dwt_analysis_stage(spectrum: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarray:
+    """Per-cluster forward DWT and scatter into l-major slots -- soft.py:134-148.
+
+    ``clusters`` (optional) restricts the stage to a subset of base pairs; untouched slots are NaN.
+    """
+    p = _plan(b)
+    bases = p.bases if clusters is None else [tuple(c) for c in clusters]
+    blocks = _pool_map(lambda bp: _forward_block(b, bp[0], bp[1], spectrum), bases, workers)
+    out = np.full(n_coeffs(b), np.nan + 0j) if clusters is not None else np.empty(n_coeffs(b), np.complex128)
+    for (bm, bmp), block in zip(bases, blocks):
+        for (m, mp, _), col in zip(cluster_members(bm, bmp), block):
+            out[pair_slots(m, mp, b)] = col
+    return out
+
+
+def dwt_synthesis_stage(coeffs: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarray:
+    """Per-cluster inverse DWT into the [m bin, j, m' bin] spectrum, Nyquist bins zero -- soft.py:154-167.
+
+    ``clusters`` (optional) restricts the stage to a subset of base pairs (other rows stay zero).
+    """
+    p = _plan(b)
+    n = p.n
+    flat = np.asarray(coeffs, dtype=np.complex128)
+    bases = p.bases if clusters is None else [tuple(c) for c in clusters]
+    blocks = _pool_map(lambda bp: _inverse_block(b, bp[0], bp[1], flat), bases, workers)
+    spectrum = np.zeros((n, n, n), dtype=np.complex128)
+    for (bm, bmp), block in zip(bases, blocks):
+        for (m, mp, _), col in zip(cluster_members(bm, bmp), block):
+            spectrum[m % n, :, mp % n] = col
+    return spectrum
+
+
+def fft_synthesis_stage(spectrum: np.ndarray, b: int, workers: int = 1) -> np.ndarray:
+    """Per-slice sign -1 DFTs into the flat [i, j, k] grid -- soft.py:169-173."""
+    n = 2 * b
+    cube = np.empty((n, n, n), dtype=np.complex128)
+    planes = _pool_map(lambda j: slice_dft(spectrum[:, j, :], -1), range(n), workers)
+    for j, plane in enumerate(planes):
+        cube[:, j, :] = plane
+    return cube.reshape(-1)
 
 
 def fsoft(grid: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarray:
@@ -328,57 +414,12 @@ def fsoft(grid: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarr
     ``clusters`` (optional) restricts the DWT stage to a subset of base pairs
     (bounded CPU-baseline samples); untouched slots are left as NaN.
     """
-    p = _plan(b)
-    n = p.n
-    cube = np.asarray(grid, dtype=np.complex128).reshape(n, n, n)
-    spectrum = np.empty((n, n, n), dtype=np.complex128)   # [m bin, j, m' bin] -- soft.py:129
-    if workers > 1:
-        planes = _pool_map(_SliceJob(cube, +1), list(range(n)), workers)
-    else:
-        planes = _slices_dft(cube, +1, range(n))
-    for j, plane in enumerate(planes):
-        spectrum[:, j, :] = plane
-    bases = p.bases if clusters is None else clusters
-    jobs = [(b, bm, bmp, [spectrum[m % n, :, mp % n] for (m, mp, _) in cluster_members(bm, bmp)])
-            for (bm, bmp) in bases]
-    results = _pool_map(_forward_cluster, jobs, workers)
-    out = np.full(n_coeffs(b), np.nan + 0j) if clusters is not None else np.empty(n_coeffs(b), np.complex128)
-    for (bm, bmp), cols in zip(bases, results):
-        for (m, mp, _), col in zip(cluster_members(bm, bmp), cols):
-            out[pair_slots(m, mp, b)] = col
-    return out
+    return dwt_analysis_stage(fft_analysis_stage(grid, b, workers), b, workers, clusters)
 
 
 def ifsoft(coeffs: np.ndarray, b: int, workers: int = 1) -> np.ndarray:
     """Inverse transform of l-major coefficients -> flat (2B)^3 grid -- soft.py:152-173."""
-    p = _plan(b)
-    n = p.n
-    flat = np.asarray(coeffs, dtype=np.complex128)
-    jobs = [(b, bm, bmp, [flat[pair_slots(m, mp, b)] for (m, mp, _) in cluster_members(bm, bmp)])
-            for (bm, bmp) in p.bases]
-    results = _pool_map(_inverse_cluster, jobs, workers)
-    spectrum = np.zeros((n, n, n), dtype=np.complex128)   # Nyquist bins stay zero -- soft.py:164
-    for (bm, bmp), cols in zip(p.bases, results):
-        for (m, mp, _), col in zip(cluster_members(bm, bmp), cols):
-            spectrum[m % n, :, mp % n] = col
-    cube = np.empty((n, n, n), dtype=np.complex128)
-    if workers > 1:
-        planes = _pool_map(_SliceJob(spectrum, -1), list(range(n)), workers)
-    else:
-        planes = _slices_dft(spectrum, -1, range(n))
-    for j, plane in enumerate(planes):
-        cube[:, j, :] = plane
-    return cube.reshape(-1)
-
-
-class _SliceJob:
-    """Picklable per-slice DFT (fork inherits the cube) -- soft.py:130, 170."""
-
-    def __init__(self, cube, sign):
-        self.cube, self.sign = cube, sign
-
-    def __call__(self, j):
-        return slice_dft(self.cube[:, j, :], self.sign)
+    return fft_synthesis_stage(dwt_synthesis_stage(coeffs, b, workers), b, workers)
 
 
 # ---------------------------------------------------------------------------

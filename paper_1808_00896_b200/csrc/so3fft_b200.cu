@@ -42,6 +42,7 @@ int fail(int code, const std::string& msg) {
   } while (0)
 
 bool valid_bandwidth(int b) { return b >= 1 && b <= 4096; }
+constexpr int kMaxBandwidth = 512;   // DWT kernels: at most 2B = 1024 beta indices per cluster
 
 // ---------------------------------------------------------------- host tables
 
@@ -547,20 +548,11 @@ int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, 
   return SO3_OK;
 }
 
-// 2B = 1024 analysis with each cluster over two 4-warp CTAs; the partial-sum scratch and the
-// counters are allocated on first use (2 x 2.86 GB at B = 512).
-int launch_dwt_ana_split(const so3_plan_s* pc, so3::DwtArgs a, unsigned ncl, cudaStream_t st) {
-  so3_plan_s* p = const_cast<so3_plan_s*>(pc);
-  if (!p->d_pbuf) {
-    const size_t pb = (size_t)2 * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2);
-    cudaError_t e = cudaMalloc((void**)&p->d_pbuf, pb);
-    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("split-analysis scratch: ") + cudaGetErrorString(e));
-    e = cudaMalloc((void**)&p->d_pcnt, (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned));
-    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("split-analysis counters: ") + cudaGetErrorString(e));
-    e = cudaMemset(p->d_pcnt, 0, (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned));
-    if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("split-analysis counters: ") + cudaGetErrorString(e));
-    p->bytes += (int64_t)pb + p->nclusters * (int64_t)sizeof(unsigned);
-  }
+// 2B = 1024 analysis with each cluster over two 4-warp CTAs.  The partial-sum scratch and the
+// arrival counters are allocated (and the counters zeroed) at plan creation, or when the
+// ana_split knob turns the split on, never on the launch path (graph capture, stream order).
+int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cudaStream_t st) {
+  if (!p->d_pbuf || !p->d_pcnt) return fail(SO3_ERR_INVALID, "split analysis without its plan scratch");
   const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
   constexpr int JW = 128;
   const int W = p->n / JW / 2;   // warps per half
@@ -703,6 +695,33 @@ int so3_cluster_schedule(int b, int32_t* bases, int32_t* members) {
 
 namespace {
 
+bool split_applies(const so3_plan_s* p) {
+  return p->ana_split && p->batch == 1 && (p->n == 1024 || (p->n == 512 && p->ana_split > 1));
+}
+
+// Split-analysis scratch: per-half partial sums (2 x rc_entries x 8) and one arrival counter
+// per cluster, allocated together (both or neither) and zeroed synchronously.
+int ensure_split_scratch(so3_plan_s* p) {
+  if (p->d_pbuf && p->d_pcnt) return SO3_OK;
+  const size_t pb = (size_t)2 * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2);
+  const size_t cb = (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned);
+  double2* buf = nullptr;
+  unsigned* cnt = nullptr;
+  cudaError_t e = cudaMalloc((void**)&buf, pb);
+  e = e ? e : cudaMalloc((void**)&cnt, cb);
+  e = e ? e : cudaMemset(cnt, 0, cb);
+  e = e ? e : cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(buf);
+    cudaFree(cnt);
+    return fail(SO3_ERR_NOMEM, std::string("split-analysis scratch: ") + cudaGetErrorString(e));
+  }
+  p->d_pbuf = buf;
+  p->d_pcnt = cnt;
+  p->bytes += (int64_t)(pb + cb);
+  return SO3_OK;
+}
+
 // Tables and buffers of a plan over the cluster list `cl` (all clusters, or one rank's group).
 int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   const int b = p->B, n = p->n, batch = p->batch;
@@ -780,6 +799,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   }
   e = e ? e : cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  if (split_applies(p)) return ensure_split_scratch(p);
   return SO3_OK;
 }
 
@@ -792,9 +812,6 @@ so3_plan_s* new_plan(int b, int batch) {
   p->ngrid = so3_grid_count(b);
   p->J = p->n;
   cudaGetDevice(&p->device);
-  if (const char* e = getenv("SO3_FFT_XB")) p->fft_wide = atoi(e);
-  if (const char* e = getenv("SO3_SYN_JW")) p->syn_jw = atoi(e);
-  if (const char* e = getenv("SO3_DWT_VARIANT")) p->dwt_variant = atoi(e);
   return p;
 }
 
@@ -807,7 +824,10 @@ int so3_plan_create(int b, int batch, so3_plan_t* out) {
   *out = nullptr;
   if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
   if (batch < 1) return fail(SO3_ERR_INVALID, "batch must be >= 1, got " + std::to_string(batch));
-  if (b > 1024) return fail(SO3_ERR_INVALID, "bandwidth > 1024 does not fit one device");
+  if (b > kMaxBandwidth)
+    return fail(SO3_ERR_INVALID, "bandwidth must be <= " + std::to_string(kMaxBandwidth) +
+                                     " (the DWT kernels span at most 2B = 1024 beta indices per cluster), got " +
+                                     std::to_string(b));
   so3_plan_s* p = new_plan(b, batch);
   const int rc = build_plan(p, host_clusters(b));
   if (rc) { so3_plan_destroy(p); return rc; }
@@ -822,7 +842,8 @@ int so3_shard_plan_create(int b, int world, int rank, so3_plan_t* out) {
 int so3_shard_plan_create_chunked(int b, int world, int rank, int chunks, so3_plan_t* out) {
   if (!out) return fail(SO3_ERR_INVALID, "null plan output");
   *out = nullptr;
-  if (!valid_bandwidth(b) || b > 1024) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 1024], got " + std::to_string(b));
+  if (!valid_bandwidth(b) || b > kMaxBandwidth)
+    return fail(SO3_ERR_INVALID, "bandwidth must be in [1, " + std::to_string(kMaxBandwidth) + "], got " + std::to_string(b));
   if (world < 1 || rank < 0 || rank >= world) return fail(SO3_ERR_INVALID, "rank outside [0, world)");
   if ((2 * b) % world) return fail(SO3_ERR_INVALID, "2B must be divisible by the number of ranks");
   if (chunks < 1 || chunks > 64) return fail(SO3_ERR_INVALID, "chunks must be in [1, 64]");
@@ -964,7 +985,14 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   const std::string k(name);
   if (k == "dwt_variant") return so3_plan_set_dwt_variant(p, value);
   if (k == "syn_jw") { p->syn_jw = value; return SO3_OK; }
-  if (k == "ana_split") { p->ana_split = value; return SO3_OK; }
+  if (k == "ana_split") {
+    const int old = p->ana_split;
+    p->ana_split = value;
+    if (split_applies(p)) {
+      if (int rc = ensure_split_scratch(p)) { p->ana_split = old; return rc; }
+    }
+    return SO3_OK;
+  }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
   if (k == "fft_fused") { p->fft_fused = value; return SO3_OK; }

@@ -204,6 +204,17 @@ def _torch():
     return torch
 
 
+def _resolve_device(device):
+    """'cuda' / None -> the CURRENT CUDA device (torch's own convention), 'cuda:k' / k -> device k."""
+    torch = _torch()
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+    if d.type != "cuda":
+        raise ValueError(f"so3fft_b200 plans live on a CUDA device, got {device!r}")
+    return torch.device("cuda", torch.cuda.current_device() if d.index is None else d.index)
+
+
 class TransformPlan:
     """Reusable per-bandwidth GPU state (reference soft.py:56-77).
 
@@ -222,8 +233,7 @@ class TransformPlan:
         self.batch = batch
         if not torch.cuda.is_available():
             raise RuntimeError("so3fft_b200 needs a CUDA device (there is no CPU path)")
-        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
-                                   torch.device(device).index or 0)
+        self.device = _resolve_device(device)
         self.matrices = None
         self.angles = sample_angles(bandwidth)
         self.weights = quadrature_weights(bandwidth)
@@ -470,14 +480,16 @@ def fft_analysis(plan: TransformPlan, samples, spectrum) -> None:
     """K1: weighted torus spectrum spectrum[f][m'][m][j] of device samples (fft.py:72-76, soft.py:130-132)."""
     ps = _device_buffer(samples, _grid_count(plan), plan, "samples")
     pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
-    _native.check(_native.lib().so3_fft_analysis(plan.handle, ps, pz, _stream(plan)), "fft_analysis")
+    with _torch().cuda.device(plan.device):
+        _native.check(_native.lib().so3_fft_analysis(plan.handle, ps, pz, _stream(plan)), "fft_analysis")
 
 
 def fft_synthesis(plan: TransformPlan, spectrum, samples) -> None:
     """K4: samples from spectrum[f][m'][m][j] (soft.py:164-172); spectrum is read only."""
     pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
     ps = _device_buffer(samples, _grid_count(plan), plan, "samples")
-    _native.check(_native.lib().so3_fft_synthesis(plan.handle, pz, ps, _stream(plan)), "fft_synthesis")
+    with _torch().cuda.device(plan.device):
+        _native.check(_native.lib().so3_fft_synthesis(plan.handle, pz, ps, _stream(plan)), "fft_synthesis")
 
 
 def dwt_analysis(plan: TransformPlan, spectrum, coeffs, begin: int = 0, end: int | None = None) -> None:
@@ -485,7 +497,8 @@ def dwt_analysis(plan: TransformPlan, spectrum, coeffs, begin: int = 0, end: int
     end = plan.n_clusters if end is None else end
     pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
     pc = _device_buffer(coeffs, _coef_count(plan), plan, "coeffs")
-    _native.check(_native.lib().so3_dwt_analysis(plan.handle, pz, pc, begin, end, _stream(plan)), "dwt_analysis")
+    with _torch().cuda.device(plan.device):
+        _native.check(_native.lib().so3_dwt_analysis(plan.handle, pz, pc, begin, end, _stream(plan)), "dwt_analysis")
 
 
 def dwt_synthesis(plan: TransformPlan, coeffs, spectrum, begin: int = 0, end: int | None = None) -> None:
@@ -493,7 +506,8 @@ def dwt_synthesis(plan: TransformPlan, coeffs, spectrum, begin: int = 0, end: in
     end = plan.n_clusters if end is None else end
     pc = _device_buffer(coeffs, _coef_count(plan), plan, "coeffs")
     pz = _device_buffer(spectrum, _grid_count(plan), plan, "spectrum")
-    _native.check(_native.lib().so3_dwt_synthesis(plan.handle, pc, pz, begin, end, _stream(plan)), "dwt_synthesis")
+    with _torch().cuda.device(plan.device):
+        _native.check(_native.lib().so3_dwt_synthesis(plan.handle, pc, pz, begin, end, _stream(plan)), "dwt_synthesis")
 
 
 def wigner_rows(plan: TransformPlan, m: int, mp: int):
@@ -505,7 +519,8 @@ def wigner_rows(plan: TransformPlan, m: int, mp: int):
     if lo >= b:
         raise ValueError(f"order pair (m={m}, m'={mp}) has no degrees below B={b}")
     out = torch.empty((b - lo, 2 * b), dtype=torch.float64, device=plan.device)
-    _native.check(_native.lib().so3_wigner_rows(plan.handle, m, mp, _ptr(out), _stream(plan)), "wigner_rows")
+    with _torch().cuda.device(plan.device):
+        _native.check(_native.lib().so3_wigner_rows(plan.handle, m, mp, _ptr(out), _stream(plan)), "wigner_rows")
     return out
 
 
