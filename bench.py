@@ -130,98 +130,116 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU baseline (oracle port)
 
-_POOL_DATA = None
+CPU_WHOLE = os.path.join(ROOT, "profiles", "r02_cpu_whole.json")
 
 
-def _slice_job(j):
-    from oracle import so3_oracle as O
-    cube, sign = _POOL_DATA["cube"], _POOL_DATA["sign"]
-    return O.slice_dft(cube[:, j, :], sign)
+class ReferenceSample:
+    """A bounded, proportional sample of one iFSOFT + FSOFT of the reference arithmetic.
 
-
-def _cluster_job(i):
-    from oracle import so3_oracle as O
-    fn = O._inverse_cluster if _POOL_DATA["direction"] == "inverse" else O._forward_cluster
-    return fn(_POOL_DATA["jobs"][i])
-
-
-def _timed_pool_map(fn, count: int, workers: int) -> float:
-    """Fork a pool (outside the timed region), time map(fn, range(count)) on it."""
-    import multiprocessing as mp
-    if workers <= 1:
-        t0 = time.perf_counter()
-        for i in range(count):
-            fn(i)
-        return time.perf_counter() - t0
-    with mp.get_context("fork").Pool(processes=workers) as pool:
-        pool.map(abs, range(workers))           # workers are up before the clock starts
-        t0 = time.perf_counter()
-        pool.map(fn, range(count), chunksize=max(1, count // (workers * 4)))
-        return time.perf_counter() - t0
-
-
-def cpu_sample_rate(b: int, seed: int, workers: int, slice_sample: int, cluster_sample: int) -> dict:
-    """Time the oracle (numpy restatement of the reference, oracle/so3_oracle.py) on a bounded
-    random sample of the B workload on a fork pool of `workers` processes (the reference's
-    own parallel scheme, schedule.py:200-248), and extrapolate to whole transforms.
-
-    Per direction: slice DFTs of `slice_sample` random beta slices (x 2B / sample) plus the
-    DWT work items of `cluster_sample` random symmetry clusters (x clusters / sample; the
-    mean of a uniform sample is unbiased for the total).  Pool start-up is not timed.
+    The oracle (oracle/so3_oracle.py, bit-identical to the reference) runs its four stages
+    exactly as the reference's *_parallel does (soft.py:124-173 over run_items,
+    schedule.py:200-257: a fork pool per stage, fork-inherited items, dynamic batches, the
+    parent-side transpose / scatter into freshly allocated outputs), but on 1/`stride` of the
+    work: every stride-th beta slice for the two FFT stages and every stride-th symmetry cluster
+    in (m, m') order for the two DWT stages (systematic samples with a per-step offset, so
+    every cluster size is represented).  Each stage's time is scaled by its own sampling
+    fraction to a whole-transform estimate.  A step is therefore ~1/stride of a transform
+    pair, and the line's value = transforms_per_step / step time is consistent with its
+    ms_per_step.  profiles/r02_cpu_whole.json holds WHOLE measured runs (B = 64..512 on the
+    GPU box's 16 cores) that calibrate this estimate.
     """
-    global _POOL_DATA
-    from oracle import so3_oracle as O
-    n = 2 * b
-    rng = np.random.default_rng(seed)
-    bases = O.base_pairs(b)
-    ks = rng.choice(len(bases), size=min(cluster_sample, len(bases)), replace=False)
-    sample_bases = [bases[k] for k in sorted(ks)]
-    nsl = min(slice_sample, n)
-    cube = rng.standard_normal((n, nsl, n)) + 1j * rng.standard_normal((n, nsl, n))
-    O._plan(b)   # plan tables outside the timed region (reference bench.py:156-158)
-    t = {}
-    for direction, sign in (("inverse", -1), ("forward", +1)):
-        _POOL_DATA = {"cube": cube, "sign": sign}
-        t_fft = _timed_pool_map(_slice_job, nsl, workers) * n / nsl
-        jobs = []
-        for (bm, bmp) in sample_bases:
-            mem = O.cluster_members(bm, bmp)
-            k = b - bm
-            size = k if direction == "inverse" else n
-            jobs.append((b, bm, bmp, [rng.standard_normal(size) + 1j * rng.standard_normal(size) for _ in mem]))
-        _POOL_DATA = {"jobs": jobs, "direction": direction}
-        t_dwt = _timed_pool_map(_cluster_job, len(jobs), workers) * len(bases) / len(jobs)
-        t[direction] = t_fft + t_dwt
-        t[direction + "_fft_s"] = t_fft
-        t[direction + "_dwt_s"] = t_dwt
-    _POOL_DATA = None
-    t["transforms_per_s"] = 2.0 / (t["inverse"] + t["forward"])
-    t["sample"] = (f"B={b}: {nsl}/{n} beta slices and {len(jobs)}/{len(bases)} symmetry clusters per direction "
-                   f"(random, seed {seed}) on a {workers}-process fork pool, extrapolated to whole iFSOFT+FSOFT")
-    return t
+
+    def __init__(self, b: int, workers: int, stride: int):
+        from oracle import so3_oracle as O
+        self.O, self.b, self.n, self.workers, self.stride = O, b, 2 * b, workers, max(1, stride)
+        n = self.n
+        O._plan(b)   # plan tables outside the timed region (reference bench.py:156-158)
+        self.c = seeded_coefficients(b, b)
+        self.bases = sorted(O.base_pairs(b))
+        # stage inputs are fully populated, as in a whole run (the forked workers then read
+        # shared pages instead of faulting in zero pages); outputs are fresh per step
+        self.grid = np.full((n, n, n), 0.5 - 0.25j, dtype=np.complex128)
+        self.spec_in = np.full((n, n, n), 0.25 + 0.5j, dtype=np.complex128)
+
+    def step(self, k: int) -> dict:
+        O, b, n, st = self.O, self.b, self.n, self.stride
+        js = list(range(k % st, n, st))
+        cl = self.bases[k % st::st]
+        # the per-stage fixed cost (fork a pool of this process, start its workers, collect) is
+        # paid once per stage by a whole run too: measured here, and not scaled
+        p0 = time.perf_counter()
+        O._pool_map(lambda i: i, range(4 * self.workers), self.workers)
+        ovh = time.perf_counter() - p0
+        t = {"pool_overhead_s": ovh}
+        t0 = time.perf_counter()
+        O.dwt_synthesis_stage(self.c, b, self.workers, clusters=cl, out=np.zeros((n, n, n), dtype=np.complex128))
+        t1 = time.perf_counter()
+        O.fft_synthesis_stage(self.spec_in, b, self.workers, slices=js, out=np.empty(n ** 3, dtype=np.complex128))
+        t2 = time.perf_counter()
+        O.fft_analysis_stage(self.grid, b, self.workers, slices=js, out=np.empty((n, n, n), dtype=np.complex128))
+        t3 = time.perf_counter()
+        O.dwt_analysis_stage(self.spec_in, b, self.workers, clusters=cl,
+                             out=np.empty(O.n_coeffs(b), dtype=np.complex128))
+        t4 = time.perf_counter()
+        fs, fc = len(js) / n, len(cl) / len(self.bases)
+        t["sample_s"] = t4 - t0
+        t["stages_sample_s"] = {"dwt_synthesis": t1 - t0, "fft_synthesis": t2 - t1, "fft_analysis": t3 - t2,
+                                "dwt_analysis": t4 - t3}
+        scale = lambda dt, f: ovh + max(dt - ovh, 0.0) / f
+        t["inverse_s"] = scale(t1 - t0, fc) + scale(t2 - t1, fs)
+        t["forward_s"] = scale(t3 - t2, fs) + scale(t4 - t3, fc)
+        t["transforms_per_s"] = 2.0 / (t["inverse_s"] + t["forward_s"])
+        t["transforms_per_step"] = t["transforms_per_s"] * t["sample_s"]
+        t["sample"] = (f"B={b}: {len(js)}/{n} beta slices and {len(cl)}/{len(self.bases)} symmetry clusters "
+                       f"(systematic, offset {k % st}) through all four stages of iFSOFT + FSOFT on a "
+                       f"{self.workers}-process fork pool; stage times less the measured pool start-up scaled by their sampling fractions")
+        return t
+
+
+def cpu_whole_measured(b: int):
+    """Whole measured runs of the reference arithmetic (profiles/r02_cpu_whole.json)."""
+    if not os.path.exists(CPU_WHOLE):
+        return None
+    with open(CPU_WHOLE) as fh:
+        rec = json.load(fh)
+    run = rec["runs"].get(f"B{b}")
+    if run is None:
+        return None
+    return {"transforms_per_s": run["transforms_per_s"], "inverse_s": run["inverse_s"],
+            "forward_s": run["forward_s"], "cores": run["cores"], "host": rec["host"],
+            "source": "profiles/r02_cpu_whole.json (tools/parity_full.py)"}
 
 
 def run_reference_arm(args, rank: int, world: int) -> None:
-    """--impl reference: the oracle port of the reference path on all host cores, rank 0 only."""
+    """--impl reference: the reference arithmetic (oracle port) on all host cores, rank 0 only.
+    Each warm-up or timed step is one bounded ReferenceSample step."""
     if rank != 0:
         return
     from oracle import so3_oracle as O
     b = args.bandwidth
     workers = O.default_workers()
-    rates, samples = [], None
-    for s in range(args.warmup + args.steps):
-        r = cpu_sample_rate(b, 7000 + s, workers, args.cpu_slices, args.cpu_clusters)
-        if s >= args.warmup:
-            rates.append(r["transforms_per_s"])
-            samples = r["sample"]
-    v = statistics.mean(rates)
+    smp = ReferenceSample(b, workers, args.cpu_stride)
+    for k in range(args.warmup):
+        smp.step(k)
+    steps = [smp.step(args.warmup + k) for k in range(args.steps)]
+    total_s = sum(r["sample_s"] for r in steps)
+    per_step = sum(r["transforms_per_step"] for r in steps) / len(steps)
+    v = per_step * len(steps) / total_s
+    whole = cpu_whole_measured(b)
+    cpu = {"value": v, "unit": "transforms/s", "cores": workers, "kind": "port", "sample": steps[-1]["sample"],
+           "extrapolated": True, "transforms_per_step": per_step,
+           "est_seconds": {"inverse": statistics.mean(r["inverse_s"] for r in steps),
+                           "forward": statistics.mean(r["forward_s"] for r in steps)}}
+    if whole:
+        cpu["measured_whole"] = whole
+        cpu["estimate_over_measured"] = v / whole["transforms_per_s"]
     line = {
         "impl": "reference", "metric": metric_name(b), "value": v, "unit": "transforms/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 2000.0 / v, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "ms_per_step": 1000.0 * total_s / len(steps), "transforms_per_step": per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(b, world),
-        "cpu_baseline": {"value": v, "unit": "transforms/s", "cores": workers, "kind": "port", "sample": samples},
+        "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -427,12 +445,16 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
                                 if dom.startswith("dwt") else
                                 f"256*B^3 x {F} functions = {alg:.4g} bytes per direction (grid read + write)")}
     cpu = None
-    if world == 1 and not args.no_cpu:
+    if world == 1 and not args.no_cpu and F == 1:
         from oracle import so3_oracle as O
-        r = cpu_sample_rate(b, 4242, O.default_workers(), args.cpu_slices, args.cpu_clusters)   # per function
+        r = ReferenceSample(b, O.default_workers(), args.cpu_stride).step(0)   # one bounded step
         cpu = {"value": r["transforms_per_s"], "unit": "transforms/s", "cores": O.default_workers(),
-               "kind": "port", "sample": r["sample"],
-               "est_seconds": {"inverse": r["inverse"], "forward": r["forward"]}}
+               "kind": "port", "sample": r["sample"], "extrapolated": True, "sample_s": r["sample_s"],
+               "est_seconds": {"inverse": r["inverse_s"], "forward": r["forward_s"]}}
+        whole = cpu_whole_measured(b)
+        if whole:
+            cpu["measured_whole"] = whole
+            cpu["estimate_over_measured"] = r["transforms_per_s"] / whole["transforms_per_s"]
     line = {
         "metric": metric_name(b, F), "value": value, "unit": "transforms/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -668,11 +690,14 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-slices", type=int, default=64)
-    ap.add_argument("--cpu-clusters", type=int, default=2048)
+    ap.add_argument("--cpu-stride", type=int, default=0,
+                    help="CPU sample: every k-th beta slice and cluster per step (0 = auto: ~1/32 of a transform "
+                         "pair at B=512, whole transforms at B <= 128)")
     ap.add_argument("--launch-check", action="store_true",
                     help="rendezvous only (gloo): every rank reports in, rank 0 prints the ranks it saw")
     args = ap.parse_args()
+    if args.cpu_stride <= 0:
+        args.cpu_stride = {512: 32, 256: 4}.get(args.bandwidth, 1)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules require >= 3 warm-up steps", file=sys.stderr)
 

@@ -210,6 +210,19 @@ int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_de
 int so3_fsoft_direct(int bandwidth, const void* samples_dev, void* coeffs_dev, void* stream);
 int so3_ifsoft_direct(int bandwidth, const void* coeffs_dev, void* samples_dev, void* stream);
 
+/* ---- Wigner utilities at arbitrary angles (the reference's wigner.py surface) ----------
+ * One thread per point; beta_dev / x_dev / out_dev are device arrays of `count` doubles
+ * (rows: (B-L) x count).  Argument checks as the reference (ValueError -> SO3_ERR_INVALID);
+ * the caller checks beta in [0, pi] and |x| <= 1 as wigner.py:71-76 / 53-54. */
+/* jacobi_poly (wigner.py:43-68) */
+int so3_jacobi_eval(int n, double a, double b, const double* x_dev, int64_t count, double* out_dev, void* stream);
+/* wigner_d_direct (wigner.py:92-114): closed form after canonicalisation to m' >= |m| */
+int so3_wigner_d_eval(int l, int m, int mp, const double* beta_dev, int64_t count, double* out_dev, void* stream);
+/* wigner_d_rows (wigner.py:139-178): seed (wigner.py:117-136) + three-term recurrence,
+ * out_dev[(l - L) * count + i], L = max(|m|, |m'|) */
+int so3_wigner_rows_eval(int bandwidth, int m, int mp, const double* beta_dev, int64_t count, double* out_dev,
+                         void* stream);
+
 /* Wigner rows d^l_{m,m'}(beta_j), l = max(|m|,|m'|)..B-1, j < 2B, for any pair
  * (wigner_d_rows, wigner.py:139-178 + derive_cluster_matrices, dwt.py:76-93):
  * out_dev[(l-L)*2B + j], generated by the same in-register recurrence as the DWT. */

@@ -233,6 +233,47 @@ def run_parity(b: int, so3, torch, *, workers: int = 1, truth_slices=(0,), truth
                                                  cd.abs()[int(torch.argmax(dg / cd.abs()))]),
         "min_abs_coefficient": float(cd.abs().min()),
     }
+    # the per-slot distribution, not only its single largest entry (which sits at the smallest
+    # |c| of the draw for both implementations)
+    ca = cd.abs()
+    for name, d in (("gpu", dg), ("reference", dr)):
+        per = torch.sort(d / ca).values
+        k = per.numel()
+        res["round_trip_compare"][f"{name}_per_slot_quantiles"] = {
+            q: float(per[min(k - 1, int(float(q) * k))]) for q in ("0.5", "0.99", "0.999", "0.9999", "0.99999")}
+        res["round_trip_compare"][f"{name}_slots_over_1e-10"] = int((per > 1e-10).sum())
+        del per
+    del ca
+    # ---------------- the fp64 floor of the round trip: the grid itself is fp64
+    # g_gpu holds the band-limited function rounded to fp64.  Moving every component by one
+    # ulp in a random direction (a perturbation of the size of that rounding; uniform rounding
+    # error has rms ulp/sqrt(12)) and transforming again shows the coefficient error that no
+    # fp64-grid implementation can avoid, slot by slot.
+    gen = torch.Generator(device=dev).manual_seed(1234)
+    gv = torch.view_as_real(g_gpu).reshape(-1)
+    pert = torch.empty_like(gv)
+    inf = torch.tensor(float("inf"), dtype=torch.float64, device=dev)
+    for s0 in range(0, gv.numel(), 1 << 27):
+        x = gv[s0:s0 + (1 << 27)]
+        up = torch.rand(x.shape, generator=gen, device=dev, dtype=torch.float64) < 0.5
+        pert[s0:s0 + (1 << 27)] = torch.where(up, torch.nextafter(x, inf), torch.nextafter(x, -inf))
+    del up, x
+    pert = pert.view(-1, 2)
+    f_pert = so3.fsoft_sequential(so3.So3SampleGrid(b, torch.view_as_complex(pert)), plan).data
+    del pert
+    dp = (f_pert - f_rt).abs()
+    ca = cd.abs()
+    imin = int(torch.argmin(ca))
+    res["grid_ulp_floor"] = {
+        "what": "coefficients of fsoft(grid moved by 1 ulp per component, random sign) - fsoft(grid)",
+        "max_abs": float(dp.max()), "rms_abs": float(dp.pow(2).mean().sqrt()),
+        "per_slot": float((dp / ca).max()),
+        "per_slot_at_min_abs_coefficient": float(dp[imin] / ca[imin]),
+        "rounding_scale": 1.0 / 12 ** 0.5,
+        "expected_rounding_per_slot_at_min_abs_coefficient": float(dp[imin] / ca[imin]) / 12 ** 0.5,
+        "expected_rounding_rms_abs": float(dp.pow(2).mean().sqrt()) / 12 ** 0.5,
+    }
+    del f_pert, dp
     res["oracle_seconds"] = times
     res["oracle_inverse_s"] = times["dwt_synthesis"] + times["fft_synthesis"]
     res["oracle_forward_s"] = times["fft_analysis"] + times["dwt_analysis"]

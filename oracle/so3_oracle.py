@@ -355,55 +355,65 @@ def _pool_map(fn, items, workers):
     return out
 
 
-def fft_analysis_stage(grid: np.ndarray, b: int, workers: int = 1) -> np.ndarray:
-    """Per-slice sign +1 DFTs into the [m bin, j, m' bin] spectrum -- soft.py:127-132."""
+def fft_analysis_stage(grid: np.ndarray, b: int, workers: int = 1, slices=None, out=None) -> np.ndarray:
+    """Per-slice sign +1 DFTs into the [m bin, j, m' bin] spectrum -- soft.py:127-132.
+
+    ``slices`` (optional) restricts the stage to those beta indices and ``out`` receives them
+    (bounded CPU-baseline samples); other slices of ``out`` are left as they are.
+    """
     n = 2 * b
     cube = np.asarray(grid, dtype=np.complex128).reshape(n, n, n)
-    spectrum = np.empty((n, n, n), dtype=np.complex128)
-    planes = _pool_map(lambda j: slice_dft(cube[:, j, :], +1), range(n), workers)
-    for j, plane in enumerate(planes):
+    spectrum = np.empty((n, n, n), dtype=np.complex128) if out is None else out
+    js = list(range(n)) if slices is None else list(slices)
+    planes = _pool_map(lambda j: slice_dft(cube[:, j, :], +1), js, workers)
+    for j, plane in zip(js, planes):
         spectrum[:, j, :] = plane
     return spectrum
 
 
-def dwt_analysis_stage(spectrum: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarray:
+def dwt_analysis_stage(spectrum: np.ndarray, b: int, workers: int = 1, clusters=None, out=None) -> np.ndarray:
     """Per-cluster forward DWT and scatter into l-major slots -- soft.py:134-148.
 
-    ``clusters`` (optional) restricts the stage to a subset of base pairs; untouched slots are NaN.
+    ``clusters`` (optional) restricts the stage to a subset of base pairs; untouched slots are
+    NaN, or left as they are in ``out``.
     """
     p = _plan(b)
     bases = p.bases if clusters is None else [tuple(c) for c in clusters]
     blocks = _pool_map(lambda bp: _forward_block(b, bp[0], bp[1], spectrum), bases, workers)
-    out = np.full(n_coeffs(b), np.nan + 0j) if clusters is not None else np.empty(n_coeffs(b), np.complex128)
+    if out is None:
+        out = np.full(n_coeffs(b), np.nan + 0j) if clusters is not None else np.empty(n_coeffs(b), np.complex128)
     for (bm, bmp), block in zip(bases, blocks):
         for (m, mp, _), col in zip(cluster_members(bm, bmp), block):
             out[pair_slots(m, mp, b)] = col
     return out
 
 
-def dwt_synthesis_stage(coeffs: np.ndarray, b: int, workers: int = 1, clusters=None) -> np.ndarray:
+def dwt_synthesis_stage(coeffs: np.ndarray, b: int, workers: int = 1, clusters=None, out=None) -> np.ndarray:
     """Per-cluster inverse DWT into the [m bin, j, m' bin] spectrum, Nyquist bins zero -- soft.py:154-167.
 
-    ``clusters`` (optional) restricts the stage to a subset of base pairs (other rows stay zero).
+    ``clusters`` (optional) restricts the stage to a subset of base pairs (other rows stay zero,
+    or as they are in ``out``).
     """
     p = _plan(b)
     n = p.n
     flat = np.asarray(coeffs, dtype=np.complex128)
     bases = p.bases if clusters is None else [tuple(c) for c in clusters]
     blocks = _pool_map(lambda bp: _inverse_block(b, bp[0], bp[1], flat), bases, workers)
-    spectrum = np.zeros((n, n, n), dtype=np.complex128)
+    spectrum = np.zeros((n, n, n), dtype=np.complex128) if out is None else out
     for (bm, bmp), block in zip(bases, blocks):
         for (m, mp, _), col in zip(cluster_members(bm, bmp), block):
             spectrum[m % n, :, mp % n] = col
     return spectrum
 
 
-def fft_synthesis_stage(spectrum: np.ndarray, b: int, workers: int = 1) -> np.ndarray:
-    """Per-slice sign -1 DFTs into the flat [i, j, k] grid -- soft.py:169-173."""
+def fft_synthesis_stage(spectrum: np.ndarray, b: int, workers: int = 1, slices=None, out=None) -> np.ndarray:
+    """Per-slice sign -1 DFTs into the flat [i, j, k] grid -- soft.py:169-173 (``slices`` / ``out``
+    as in fft_analysis_stage)."""
     n = 2 * b
-    cube = np.empty((n, n, n), dtype=np.complex128)
-    planes = _pool_map(lambda j: slice_dft(spectrum[:, j, :], -1), range(n), workers)
-    for j, plane in enumerate(planes):
+    cube = np.empty((n, n, n), dtype=np.complex128) if out is None else out.reshape(n, n, n)
+    js = list(range(n)) if slices is None else list(slices)
+    planes = _pool_map(lambda j: slice_dft(spectrum[:, j, :], -1), js, workers)
+    for j, plane in zip(js, planes):
         cube[:, j, :] = plane
     return cube.reshape(-1)
 

@@ -59,6 +59,26 @@ from .soft import (
     sigma_inverse,
     wigner_rows,
 )
+from .wigner import (
+    SYMMETRY_RELATIONS,
+    SymmetryRelation,
+    WignerColumn,
+    apply_symmetry,
+    jacobi_poly,
+    wigner_D,
+    wigner_d_column,
+    wigner_d_direct,
+    wigner_d_seed,
+)
+from .dwt import (
+    DwtScalers,
+    WignerMatrix,
+    build_wigner_matrix,
+    derive_cluster_matrices,
+    dwt_apply,
+    idwt_apply,
+    make_scalers,
+)
 from .report import (
     BenchConfig,
     BenchRecord,

@@ -111,4 +111,54 @@ __global__ void fsoft_direct_kernel(int B, const double* d, const double* w, con
   }
 }
 
+// ---- evaluation at arbitrary angles (the reference's wigner.py utilities, one thread per point)
+
+// jacobi_poly (wigner.py:43-68) at count points.
+__global__ void jacobi_eval_kernel(int nd, double a, double b, const double* x, long long count, double* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = jacobi(nd, a, b, x[i]);
+}
+
+// wigner_d_direct (wigner.py:92-114) at count angles.
+__global__ void wigner_direct_eval_kernel(int l, int m, int mp, const double* beta, long long count, double* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = wigner_closed(l, m, mp, beta[i]);
+}
+
+// wigner_d_rows (wigner.py:139-178) for ANY pair at count angles: the seed of wigner_d_seed
+// (wigner.py:117-136, norm from the host) and the three-term recurrence in the reference's
+// operation order; out[(l - L) * count + i].
+__global__ void wigner_rows_eval_kernel(int B, int m, int mp, double norm, const double* beta, long long count,
+                                        double* out) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double bt = beta[i];
+  double s, c;
+  sincos(0.5 * bt, &s, &c);
+  double cur;
+  const int am = abs(m), amp = abs(mp);
+  if (am >= amp) cur = m >= 0 ? norm * pow(c, (double)(am + mp)) * pow(s, (double)(am - mp))
+                              : norm * pow(c, (double)(am - mp)) * pow(-s, (double)(am + mp));
+  else cur = mp >= 0 ? norm * pow(c, (double)(amp + m)) * pow(-s, (double)(amp - m))
+                     : norm * pow(c, (double)(amp - m)) * pow(s, (double)(amp + m));
+  const int L = max(am, amp);
+  const double x = cos(bt);
+  double prev = 0.0;
+  out[i] = cur;
+  for (int l = L; l < B - 1; ++l) {
+    const double lp = l + 1.0;
+    const double denom = sqrt((lp * lp - (double)m * m) * (lp * lp - (double)mp * mp));
+    const double al = lp * (2.0 * l + 1.0) / denom;
+    double shift = 0.0, cl = 0.0;
+    if (l > 0) {
+      shift = ((double)m * mp) / ((double)l * lp);
+      cl = lp * sqrt(((double)l * l - (double)m * m) * ((double)l * l - (double)mp * mp)) / ((double)l * denom);
+    }
+    const double nx = al * (x - shift) * cur - cl * prev;
+    out[(long long)(l + 1 - L) * count + i] = nx;
+    prev = cur;
+    cur = nx;
+  }
+}
+
 }  // namespace so3

@@ -1225,6 +1225,48 @@ int so3_fsoft_direct(int b, const void* samples, void* coeffs, void* stream) {
   return rc;
 }
 
+static unsigned blocks_for(long long count) { return (unsigned)((count + 255) / 256); }
+
+int so3_jacobi_eval(int n, double a, double b, const double* x, int64_t count, double* out, void* stream) {
+  if (n < 0) return fail(SO3_ERR_INVALID, "degree n must be a nonnegative integer, got " + std::to_string(n));
+  if (!(a > -1.0) || !(b > -1.0)) return fail(SO3_ERR_INVALID, "Jacobi exponents must exceed -1");
+  if (count < 0 || (count > 0 && (!x || !out))) return fail(SO3_ERR_INVALID, "bad buffers");
+  if (count == 0) return SO3_OK;
+  so3::jacobi_eval_kernel<<<blocks_for(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(n, a, b, x, count, out);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int so3_wigner_d_eval(int l, int m, int mp, const double* beta, int64_t count, double* out, void* stream) {
+  if (l < 0 || std::abs(m) > l || std::abs(mp) > l)
+    return fail(SO3_ERR_INVALID, "invalid orders (l=" + std::to_string(l) + ", m=" + std::to_string(m) +
+                                     ", m'=" + std::to_string(mp) + ")");
+  if (count < 0 || (count > 0 && (!beta || !out))) return fail(SO3_ERR_INVALID, "bad buffers");
+  if (count == 0) return SO3_OK;
+  so3::wigner_direct_eval_kernel<<<blocks_for(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(l, m, mp, beta,
+                                                                                                 count, out);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int so3_wigner_rows_eval(int b, int m, int mp, const double* beta, int64_t count, double* out, void* stream) {
+  if (!valid_bandwidth(b)) return fail(SO3_ERR_INVALID, "bandwidth must be in [1, 4096], got " + std::to_string(b));
+  const int L = std::max(std::abs(m), std::abs(mp));
+  if (L >= b)
+    return fail(SO3_ERR_INVALID, "order pair (m=" + std::to_string(m) + ", m'=" + std::to_string(mp) +
+                                     ") has no degrees below B=" + std::to_string(b));
+  if (count < 0 || (count > 0 && (!beta || !out))) return fail(SO3_ERR_INVALID, "bad buffers");
+  if (count == 0) return SO3_OK;
+  // norm of wigner_d_seed (wigner.py:124/131) in the reference's own double arithmetic
+  const int big = std::max(std::abs(m), std::abs(mp)), o = std::abs(m) >= std::abs(mp) ? mp : m;
+  const double norm = std::exp(0.5 * (std::lgamma(2.0 * big + 1) - std::lgamma((double)big + o + 1) -
+                                      std::lgamma((double)big - o + 1)));
+  so3::wigner_rows_eval_kernel<<<blocks_for(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(b, m, mp, norm,
+                                                                                               beta, count, out);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 int so3_wigner_rows(so3_plan_t p, int m, int mp, double* out, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(out);
   const int L = std::max(std::abs(m), std::abs(mp));

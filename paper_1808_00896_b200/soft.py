@@ -19,11 +19,13 @@ from __future__ import annotations
 import ctypes
 import math
 from dataclasses import dataclass, field
+from collections.abc import Mapping
 from typing import Any, NamedTuple
 
 import numpy as np
 
 from . import _native
+from .wigner import SYMMETRY_RELATIONS
 from .core import (
     So3Coefficients,
     So3SampleGrid,
@@ -52,16 +54,10 @@ _TAGS = {
     "full": ("identity", "negate_both", "swap", "swap_negate_both",
              "negate_m", "negate_mp", "swap_negate_m", "swap_negate_mp"),
 }
-# target map (tm_m, tm_mp, tp_m, tp_mp) per tag, reference wigner.py:244-256
-_TARGET = {
-    "identity": (1, 0, 0, 1), "negate_both": (-1, 0, 0, -1), "swap": (0, 1, 1, 0),
-    "swap_negate_both": (0, -1, -1, 0), "negate_m": (-1, 0, 0, 1), "negate_mp": (1, 0, 0, -1),
-    "swap_negate_m": (0, -1, 1, 0), "swap_negate_mp": (0, 1, -1, 0),
-}
 
 
 class SymmetryCluster(NamedTuple):
-    """Base pair and its orbit (reference schedule.py:93-103); members are (pair, tag)."""
+    """Base pair and its orbit (reference schedule.py:93-103); members are (pair, SymmetryRelation)."""
     kind: str
     base: OrderPair
     members: tuple
@@ -74,8 +70,8 @@ def cluster_for_base(m: int, mp: int) -> SymmetryCluster:
     kind = "origin" if m == 0 else "axis" if mp == 0 else "diagonal" if mp == m else "full"
     members = []
     for tag in _TAGS[kind]:
-        a, b, c, d = _TARGET[tag]
-        members.append((OrderPair(a * m + b * mp, c * m + d * mp), tag))
+        rel = SYMMETRY_RELATIONS[tag]
+        members.append((OrderPair(*rel.target(m, mp)), rel))
     return SymmetryCluster(kind, OrderPair(m, mp), tuple(members))
 
 
@@ -215,14 +211,46 @@ def _resolve_device(device):
     return torch.device("cuda", torch.cuda.current_device() if d.index is None else d.index)
 
 
+class _MatrixTable(Mapping):
+    """plan.matrices of a "precomputed" plan (soft.py:100-106): OrderPair -> WignerMatrix of every
+    order pair, computed on access by the GPU recurrence (dwt.build_wigner_matrix +
+    derive_cluster_matrices) and cached per cluster for the last few clusters."""
+
+    def __init__(self, plan):
+        self._plan = plan
+        self._cache: dict = {}
+
+    def __getitem__(self, pair):
+        from .dwt import build_wigner_matrix, derive_cluster_matrices
+        m, mp = int(pair[0]), int(pair[1])
+        b = self._plan.bandwidth
+        if max(abs(m), abs(mp)) >= b:
+            raise KeyError(pair)
+        base = (max(abs(m), abs(mp)), min(abs(m), abs(mp)))
+        if base not in self._cache:
+            if len(self._cache) >= 8:
+                self._cache.pop(next(iter(self._cache)))
+            mats = derive_cluster_matrices(build_wigner_matrix(*base, b, self._plan.angles.betas),
+                                           cluster_for_base(*base))
+            self._cache[base] = mats
+        return self._cache[base][OrderPair(m, mp)]
+
+    def __iter__(self):
+        b = self._plan.bandwidth
+        return (OrderPair(m, mp) for m in range(-b + 1, b) for mp in range(-b + 1, b))
+
+    def __len__(self):
+        return (2 * self._plan.bandwidth - 1) ** 2
+
+
 class TransformPlan:
     """Reusable per-bandwidth GPU state (reference soft.py:56-77).
 
     Holds the native plan (beta tables, weights, twiddles, cluster schedule,
     scratch spectrum) on one CUDA device.  ``matrix_policy`` is accepted for API
     compatibility; Wigner matrices are never stored (they are regenerated in
-    registers by the recurrence), so "precomputed" computes the same values and
-    ``matrices`` is always None.
+    registers by the recurrence), so "precomputed" computes the same values; its
+    ``matrices`` mapping serves each pair's matrix on access instead of storing the table.
     """
 
     def __init__(self, bandwidth: int, matrix_policy: str, partitioner: str, batch: int, device):
@@ -234,8 +262,11 @@ class TransformPlan:
         if not torch.cuda.is_available():
             raise RuntimeError("so3fft_b200 needs a CUDA device (there is no CPU path)")
         self.device = _resolve_device(device)
-        self.matrices = None
         self.angles = sample_angles(bandwidth)
+        # "precomputed": the per-pair matrices are served on access (GPU recurrence), never
+        # stored -- the reference's table is 1.47 TB at B = 512, and the kernels regenerate the
+        # rows in registers faster than they could stream them
+        self.matrices = _MatrixTable(self) if matrix_policy == "precomputed" else None
         self.weights = quadrature_weights(bandwidth)
         self.degree_scale = degree_scale(bandwidth)
         self._clusters = None

@@ -155,6 +155,36 @@ def test_sampled_oracle_at_b512():
             assert rel_of_max(mine, col) < 1e-12, (m, mp)
 
 
+def test_sampled_inverse_oracle_at_b512():
+    """B=512 inverse direction, sampled: DWT synthesis columns of sampled clusters against the
+    oracle's synthesis_column (dwt.py:119-125) and FFT synthesis slices against slice_dft(-1)
+    (fft.py:72-76), each fed the same input (the forward samples above do not cover K3/K4)."""
+    b, n = 512, 1024
+    plan = plan_for(b)
+    rng = np.random.default_rng(512)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    cd = torch.from_numpy(c).cuda()
+    spec = torch.zeros(n ** 3, dtype=torch.complex128, device="cuda")
+    so3.dwt_synthesis(plan, cd, spec)
+    sv = spec.view(n, n, n)                          # stored [m'][m][j]
+    betas = O.beta_nodes(b)
+    for (bm, bmp) in [(0, 0), (7, 0), (300, 300), (400, 123), (511, 510)]:
+        rows = O.recurrence_rows(bm, bmp, betas, b)
+        for (m, mp, tag) in O.cluster_members(bm, bmp):
+            ref = O.synthesis_column(O.member_matrix(rows, tag, bm, bmp, b), c[O.pair_slots(m, mp, b)])
+            assert rel_of_max(sv[mp % n, m % n, :].cpu().numpy(), ref) < 1e-12, (m, mp)
+    del cd
+    grid = torch.empty_like(spec)
+    so3.fft_synthesis(plan, spec, grid)
+    cube = grid.view(n, n, n)
+    for j in (0, 301, 1023):
+        plane = sv[:, :, j].cpu().numpy().T.copy()   # [m][m'] spectrum of slice j
+        plane[b, :] = 0.0                             # Nyquist bins read as zero (soft.py:164)
+        plane[:, b] = 0.0
+        ref = O.slice_dft(plane, -1)
+        assert rel_of_max(cube[:, j, :].cpu().numpy(), ref) < 1e-12
+
+
 # ---------------------------------------------------------------- stages and Wigner rows
 
 def test_wigner_rows_match_reference_golden(golden):
@@ -584,3 +614,58 @@ def test_split_analysis_matches_one_cta_reduction_b512():
     torch.cuda.synchronize()
     assert (outs[1] - outs[0]).abs().max().item() <= 1e-14 * outs[0].abs().max().item()
     assert torch.equal(outs[1], outs[2])
+
+
+# ---------------------------------------------------------------- wigner.py utilities (reference surface)
+
+def test_wigner_utilities_match_reference_formulas():
+    """so3fft.wigner surface on the GPU kernels: closed form vs the oracle's closed_form_d
+    (wigner.py:92-114), rows vs recurrence_rows (wigner.py:139-178) at arbitrary angles."""
+    from paper_1808_00896_b200 import wigner as W
+    beta = np.linspace(0.0, np.pi, 37)
+    for (l, m, mp) in [(0, 0, 0), (1, 1, 0), (1, 0, 1), (5, -3, 2), (9, 4, -9), (12, -12, -7)]:
+        assert np.allclose(W.wigner_d_direct(l, m, mp, beta), O.closed_form_d(l, m, mp, beta), atol=1e-13)
+    assert abs(W.wigner_d_direct(1, 1, 0, 0.3) - np.sin(0.3) / np.sqrt(2)) < 1e-15   # convention
+    for (m, mp, b) in [(0, 0, 8), (3, -2, 10), (-5, 5, 12), (7, 1, 20)]:
+        got = W.wigner_d_rows(m, mp, beta[1:-1], b)
+        ref = O.recurrence_rows(m, mp, beta[1:-1], b)
+        assert got.shape == ref.shape and np.abs(got - ref).max() < 1e-13
+        assert np.allclose(W.wigner_d_seed(m, mp, beta[1:-1]), ref[0], atol=1e-15)
+    col = W.wigner_d_column(2, 1, 0.7, 9)
+    for tag, rel in W.SYMMETRY_RELATIONS.items():
+        der = W.apply_symmetry(col, rel)
+        tm, tp = rel.target(2, 1)
+        direct = [W.wigner_d_direct(l, tm, tp, der.beta) for l in range(2, 9)]
+        assert np.allclose(der.values, direct, atol=1e-13), tag
+    x = np.linspace(-1, 1, 11)
+    assert np.allclose(W.jacobi_poly(6, 1.5, 2.0, x), O._jacobi(6, 1.5, 2.0, x), atol=1e-12)
+    assert abs(W.wigner_D(3, 1, -2, 0.2, 0.9, 1.1) -
+               np.exp(-1j * 0.2) * O.closed_form_d(3, 1, -2, 0.9) * np.exp(2j * 1.1)) < 1e-14
+    with pytest.raises(ValueError):
+        W.wigner_d_direct(2, 3, 0, 0.1)
+    with pytest.raises(ValueError):
+        W.wigner_d_rows(4, 0, beta, 4)
+    with pytest.raises(ValueError):
+        W.wigner_d_direct(2, 1, 0, 3.5)
+
+
+def test_report_harness_device_columns_and_oracles(tmp_path):
+    """report.run_benchmark (so3fft-bench schema, bench.py:146-209): identical error figures for
+    every thread count, the direct-route oracle, and device stage / roofline columns."""
+    from paper_1808_00896_b200 import report as R
+    cfg = R.BenchConfig(bandwidths=[4, 16], thread_counts=[1, 2], runs=2, seed=3, oracle=True)
+    recs = R.run_benchmark(cfg)
+    assert len(recs) == 2 * 2 * 2 * 2
+    figs = {}
+    for r in recs:
+        figs.setdefault((r.bandwidth, r.run_index, r.direction), set()).add((r.max_abs_error, r.max_rel_error))
+        assert r.max_abs_error < 1e-12
+        assert r.stages["dwt_ms"] > 0 and r.stages["fft_ms"] > 0 and 0 < r.stages["fft_frac_hbm"] < 1.5
+    assert all(len(v) == 1 for v in figs.values())
+    again = R.run_benchmark(cfg)
+    assert [(a.max_abs_error, a.max_rel_error) for a in recs] == [(b.max_abs_error, b.max_rel_error) for b in again]
+    p = tmp_path / "rep.json"
+    R.write_report(recs, str(p), "json", extended=True)
+    import json
+    rows = json.loads(p.read_text())
+    assert set(R.EXTENDED_FIELDS) <= set(rows[0]) and rows[0]["dwt_ms"] > 0

@@ -88,7 +88,7 @@ def test_enumerate_clusters_matches_reference_order(golden):
 def test_cluster_members_match_oracle():
     for b in (2, 6, 11):
         for (m, mp) in O.base_pairs(b):
-            ours = [(p.m, p.mp, tag) for p, tag in so3.cluster_for_base(m, mp).members]
+            ours = [(p.m, p.mp, rel.tag) for p, rel in so3.cluster_for_base(m, mp).members]
             assert ours == O.cluster_members(m, mp)
 
 
