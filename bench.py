@@ -156,10 +156,23 @@ class ReferenceSample:
         O._plan(b)   # plan tables outside the timed region (reference bench.py:156-158)
         self.c = seeded_coefficients(b, b)
         self.bases = sorted(O.base_pairs(b))
-        # stage inputs are fully populated, as in a whole run (the forked workers then read
-        # shared pages instead of faulting in zero pages); outputs are fresh per step
+        # Stage inputs and outputs are fully populated buffers, as a whole run's are.  A whole
+        # run also faults in its freshly allocated outputs (three (2B)^3 arrays and one
+        # coefficient array per round trip); a sample writing 1/stride of a fresh array would
+        # fault in most of its (transparent huge) pages, so that first-touch cost is measured
+        # here, on the output buffers' own first fill, and added unscaled.
         self.grid = np.full((n, n, n), 0.5 - 0.25j, dtype=np.complex128)
         self.spec_in = np.full((n, n, n), 0.25 + 0.5j, dtype=np.complex128)
+        self.spec_out = np.empty((n, n, n), dtype=np.complex128)
+        t0 = time.perf_counter()
+        self.spec_out[...] = 0.0
+        self.touch_grid_s = time.perf_counter() - t0
+        self.cube_out = np.zeros(n ** 3, dtype=np.complex128)
+        self.cube_out[...] = 0.0
+        self.coef_out = np.empty(O.n_coeffs(b), dtype=np.complex128)
+        t0 = time.perf_counter()
+        self.coef_out[...] = 0.0
+        self.touch_coef_s = time.perf_counter() - t0
 
     def step(self, k: int) -> dict:
         O, b, n, st = self.O, self.b, self.n, self.stride
@@ -172,27 +185,27 @@ class ReferenceSample:
         ovh = time.perf_counter() - p0
         t = {"pool_overhead_s": ovh}
         t0 = time.perf_counter()
-        O.dwt_synthesis_stage(self.c, b, self.workers, clusters=cl, out=np.zeros((n, n, n), dtype=np.complex128))
+        O.dwt_synthesis_stage(self.c, b, self.workers, clusters=cl, out=self.spec_out)
         t1 = time.perf_counter()
-        O.fft_synthesis_stage(self.spec_in, b, self.workers, slices=js, out=np.empty(n ** 3, dtype=np.complex128))
+        O.fft_synthesis_stage(self.spec_in, b, self.workers, slices=js, out=self.cube_out)
         t2 = time.perf_counter()
-        O.fft_analysis_stage(self.grid, b, self.workers, slices=js, out=np.empty((n, n, n), dtype=np.complex128))
+        O.fft_analysis_stage(self.grid, b, self.workers, slices=js, out=self.spec_out)
         t3 = time.perf_counter()
-        O.dwt_analysis_stage(self.spec_in, b, self.workers, clusters=cl,
-                             out=np.empty(O.n_coeffs(b), dtype=np.complex128))
+        O.dwt_analysis_stage(self.spec_in, b, self.workers, clusters=cl, out=self.coef_out)
         t4 = time.perf_counter()
         fs, fc = len(js) / n, len(cl) / len(self.bases)
         t["sample_s"] = t4 - t0
         t["stages_sample_s"] = {"dwt_synthesis": t1 - t0, "fft_synthesis": t2 - t1, "fft_analysis": t3 - t2,
                                 "dwt_analysis": t4 - t3}
         scale = lambda dt, f: ovh + max(dt - ovh, 0.0) / f
-        t["inverse_s"] = scale(t1 - t0, fc) + scale(t2 - t1, fs)
-        t["forward_s"] = scale(t3 - t2, fs) + scale(t4 - t3, fc)
+        t["first_touch_s"] = {"grid": self.touch_grid_s, "coefficients": self.touch_coef_s}
+        t["inverse_s"] = scale(t1 - t0, fc) + scale(t2 - t1, fs) + 2 * self.touch_grid_s
+        t["forward_s"] = scale(t3 - t2, fs) + scale(t4 - t3, fc) + self.touch_grid_s + self.touch_coef_s
         t["transforms_per_s"] = 2.0 / (t["inverse_s"] + t["forward_s"])
         t["transforms_per_step"] = t["transforms_per_s"] * t["sample_s"]
         t["sample"] = (f"B={b}: {len(js)}/{n} beta slices and {len(cl)}/{len(self.bases)} symmetry clusters "
                        f"(systematic, offset {k % st}) through all four stages of iFSOFT + FSOFT on a "
-                       f"{self.workers}-process fork pool; stage times less the measured pool start-up scaled by their sampling fractions")
+                       f"{self.workers}-process fork pool; stage times less the measured pool start-up scaled by their sampling fractions, plus the measured first-touch cost of the whole run's fresh outputs")
         return t
 
 

@@ -210,6 +210,23 @@ int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_de
 int so3_fsoft_direct(int bandwidth, const void* samples_dev, void* coeffs_dev, void* stream);
 int so3_ifsoft_direct(int bandwidth, const void* coeffs_dev, void* samples_dev, void* stream);
 
+/* ---- SOFC / SOFG containers (core.py:179-225), streamed ------------------------------
+ * The reference's byte format: magic "SOFC" / "SOFG", u32 version 1, u32 bandwidth, then the
+ * complex128 payload (l-major coefficients / [i][j][k] samples), little endian.
+ * kind: 0 = SOFC coefficients, 1 = SOFG samples.  For samples, [jbase, jbase + J) selects a
+ * beta slab, transferred as [i][jj][k] (J = 0: the whole grid); coefficients ignore both.
+ * Device transfers stream whole [i][jj][k] rows through two pinned bounce buffers of
+ * `staging_bytes` each (so a 17 GB grid never needs a host copy); host transfers read or write
+ * the caller's buffer directly.  Non-finite payloads are rejected on read and write, as by the
+ * reference (checked on the device for device buffers).  Synchronous on `stream`.
+ * Sharded writers: rank 0 creates the file (create = 1, sized in full), the other ranks then
+ * write their slabs with create = 0. */
+int so3_container_info(const char* path, int* kind, int* bandwidth, int64_t* elements);
+int so3_read_container(const char* path, int kind, int jbase, int J, void* dst, int dst_on_device,
+                       int64_t staging_bytes, void* stream);
+int so3_write_container(const char* path, int kind, int bandwidth, int jbase, int J, const void* src,
+                        int src_on_device, int create, int64_t staging_bytes, void* stream);
+
 /* ---- Wigner utilities at arbitrary angles (the reference's wigner.py surface) ----------
  * One thread per point; beta_dev / x_dev / out_dev are device arrays of `count` doubles
  * (rows: (B-L) x count).  Argument checks as the reference (ValueError -> SO3_ERR_INVALID);

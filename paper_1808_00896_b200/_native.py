@@ -53,6 +53,11 @@ SIGNATURES = {
     "so3_plan_set_dwt_variant": (_c_int, [_vp, _c_int]),
     "so3_plan_set_knob": (_c_int, [_vp, ctypes.c_char_p, _c_int]),
     "so3_wigner_rows": (_c_int, [_vp, _c_int, _c_int, _vp, _vp]),
+    "so3_container_info": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int),
+                                    ctypes.POINTER(_c_i64)]),
+    "so3_read_container": (_c_int, [ctypes.c_char_p, _c_int, _c_int, _c_int, _vp, _c_int, _c_i64, _vp]),
+    "so3_write_container": (_c_int, [ctypes.c_char_p, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _c_int, _c_i64,
+                                     _vp]),
     "so3_jacobi_eval": (_c_int, [_c_int, ctypes.c_double, ctypes.c_double, _vp, _c_i64, _vp, _vp]),
     "so3_wigner_d_eval": (_c_int, [_c_int, _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
     "so3_wigner_rows_eval": (_c_int, [_c_int, _c_int, _c_int, _vp, _c_i64, _vp, _vp]),

@@ -18,6 +18,7 @@
 
 #include "../../include/so3fft_b200.h"
 #include "common.cuh"
+#include "sofio.cuh"
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
 #include "dwt_batch.cuh"
@@ -43,6 +44,19 @@ int fail(int code, const std::string& msg) {
 
 bool valid_bandwidth(int b) { return b >= 1 && b <= 4096; }
 constexpr int kMaxBandwidth = 512;   // DWT kernels: at most 2B = 1024 beta indices per cluster
+
+// Shared-memory carveout preference of the big kernels (cudaFuncAttributePreferredSharedMemory-
+// Carveout, a per-kernel, process-wide attribute; -1 = driver default).  Kernels with different
+// carveouts cannot share an SM, so concurrent FFT and DWT launches need the same one.
+int g_carveout = -1;
+
+template <typename K>
+cudaError_t set_smem(K k, size_t smem) {
+  cudaError_t e = cudaSuccess;
+  if (smem > 48 * 1024) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!e && g_carveout >= 0) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
+  return e;
+}
 
 // ---------------------------------------------------------------- host tables
 
@@ -175,6 +189,7 @@ struct so3_plan_s {
   int fft_tab_loop = 8;  // x-tiles per CTA of the sharded row-table passes (0: one tile per CTA)
   int fft_tab_tma = 1;   // row-table passes move their plain-strided side by bulk copies
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
+  int fft_pad = 0;    // extra KB of shared memory per TMA FFT pass CTA (limits FFT CTAs per SM when co-running)
 };
 
 // ------------------------------------------------------------------ launches
@@ -209,7 +224,7 @@ int launch_fft_pow2(const so3_plan_s* p, const so3::FftArgs& a, int sign, int ba
   }
   void (*k)(so3::FftArgs) = sign > 0 ? (tab ? so3::fft_pass_kernel<N, XB, +1, true> : so3::fft_pass_kernel<N, XB, +1, false>)
                                      : (tab ? so3::fft_pass_kernel<N, XB, -1, true> : so3::fft_pass_kernel<N, XB, -1, false>);
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<grid, threads, smem, st>>>(a);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -220,7 +235,7 @@ int launch_fft_direct(const so3::FftArgs& a, int sign, int batch, cudaStream_t s
   const size_t smem = (size_t)XC * a.n * sizeof(double2);
   dim3 grid((a.X + XC - 1) / XC, a.Y, batch);
   void (*k)(so3::FftArgs, int) = sign > 0 ? so3::dft_direct_kernel<+1> : so3::dft_direct_kernel<-1>;
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<grid, 256, smem, st>>>(a, XC);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -290,7 +305,7 @@ int launch_fft2d_tma_t(const so3_plan_s* p, const void* src, void* dst, cudaStre
     return -1;   // the plain slice kernel takes over
   const size_t smem = (size_t)N * so3::RowLayout<N, N>::SIZE * sizeof(double2) + 16;
   auto k = so3::fft2d_slice_tma_kernel<N, SIGN>;
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(N, p->batch), N * N / 16, smem, st>>>(map, static_cast<const double2*>(src), static_cast<double2*>(dst),
                                                  p->d_tw, p->d_w, p->ngrid, p->B);
   SO3_CUDA(cudaGetLastError());
@@ -305,7 +320,7 @@ int launch_fft2d_t(const so3_plan_s* p, const void* src, void* dst, cudaStream_t
   }
   const size_t smem = (size_t)N * so3::RowLayout<N, N>::SIZE * sizeof(double2);
   auto k = so3::fft2d_slice_kernel<N, SIGN>;
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(N, p->batch), N * N / 16, smem, st>>>(static_cast<const double2*>(src), static_cast<double2*>(dst), p->d_tw,
                                                p->d_w, p->ngrid, p->B);
   SO3_CUDA(cudaGetLastError());
@@ -340,10 +355,10 @@ int launch_fft_tstore_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, c
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.dst, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16 + (size_t)p->fft_pad * 1024;
   auto k = p->fft_bulkin ? (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1, true> : so3::fft_pass_tstore_kernel<N, XB, -1, true>)
                         : (SIGN > 0 ? so3::fft_pass_tstore_kernel<N, XB, +1> : so3::fft_pass_tstore_kernel<N, XB, -1>);
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -366,11 +381,11 @@ int launch_fft_tload_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, cu
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
-  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  const size_t smem = (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16 + (size_t)p->fft_pad * 1024;
   const bool bulkout = p->fft_bulkout < 0 ? N >= 512 : p->fft_bulkout != 0;
   auto k = bulkout ? (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1, true> : so3::fft_pass_tload_kernel<N, XB, -1, true>)
                          : (SIGN > 0 ? so3::fft_pass_tload_kernel<N, XB, +1> : so3::fft_pass_tload_kernel<N, XB, -1>);
-  if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(a.X / XB, a.Y, batch), XB * N / 16, smem, st>>>(map, a);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -493,7 +508,7 @@ int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch
   using SM = so3::MmaSmem<JW>;
   const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
   auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG>;
-  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(ncl * split, batch / FG), WPC * 32, smem, st>>>(a, split);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -505,7 +520,7 @@ int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cu
   const int warps = (n + JW - 1) / JW;
   const size_t smem = ((size_t)warps * 8 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, FG>;
-  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a, so3::SplitArgs{nullptr, 0, nullptr});
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -541,7 +556,7 @@ int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, 
     constexpr int FC = 8;
     const size_t smem = so3::batch_synthesis_smem<FC>(n);
     auto k = so3::dwt_synthesis_batch_kernel<FC, 8>;
-    SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SO3_CUDA(set_smem(k, smem));
     k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, smem, st>>>(a, batch);
   }
   SO3_CUDA(cudaGetLastError());
@@ -559,7 +574,7 @@ int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cuda
   using SM = so3::MmaSmem<JW>;
   const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double);
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
-  SO3_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  SO3_CUDA(set_smem(k, smem));
   k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a, sp);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -1001,6 +1016,16 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "fft_tab_tma") { p->fft_tab_tma = value; return SO3_OK; }
   if (k == "fft_bulkin") { p->fft_bulkin = value; return SO3_OK; }
   if (k == "fft_bulkout") { p->fft_bulkout = value; return SO3_OK; }
+  if (k == "carveout") {   // process-wide kernel attribute (see g_carveout)
+    if (value < -1 || value > 100) return fail(SO3_ERR_INVALID, "carveout must be -1 or a percentage in [0, 100]");
+    g_carveout = value;
+    return SO3_OK;
+  }
+  if (k == "fft_pad") {
+    if (value < 0 || value > 150) return fail(SO3_ERR_INVALID, "fft_pad must be in [0, 150] KB");
+    p->fft_pad = value;
+    return SO3_OK;
+  }
   return fail(SO3_ERR_INVALID, "unknown knob " + k);
 }
 
@@ -1223,6 +1248,132 @@ int so3_fsoft_direct(int b, const void* samples, void* coeffs, void* stream) {
   }
   cudaFree(be); cudaFree(w); cudaFree(tab);
   return rc;
+}
+
+// ---------------------------------------------------------------- SOFC / SOFG streaming (sofio.cuh)
+
+int so3_container_info(const char* path, int* kind, int* bandwidth, int64_t* elements) {
+  if (!path) return fail(SO3_ERR_INVALID, "null path");
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(SO3_ERR_INVALID, std::string(path) + ": " + strerror(errno));
+  so3io::Header h;
+  std::string why;
+  const int rc = so3io::parse_header(fd, path, &h, &why);
+  close(fd);
+  if (rc) return fail(rc, why);
+  if (kind) *kind = h.kind;
+  if (bandwidth) *bandwidth = h.bandwidth;
+  if (elements) *elements = h.elements;
+  return SO3_OK;
+}
+
+int so3_read_container(const char* path, int kind, int jbase, int J, void* dst, int dst_on_device,
+                       int64_t staging_bytes, void* stream) {
+  if (!path || !dst) return fail(SO3_ERR_INVALID, "null path or destination");
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return fail(SO3_ERR_INVALID, std::string(path) + ": " + strerror(errno));
+  so3io::Header h;
+  std::string why;
+  int rc = so3io::parse_header(fd, path, &h, &why);
+  if (!rc && h.kind != kind) {
+    why = std::string(path) + ": not a " + (kind ? "SOFG" : "SOFC") + " container";
+    rc = SO3_ERR_INVALID;
+  }
+  const int n = 2 * h.bandwidth;
+  if (!rc && kind == 1) {
+    if (J == 0) { jbase = 0; J = n; }
+    if (jbase < 0 || J < 1 || jbase + J > n) {
+      why = "beta slab [" + std::to_string(jbase) + ", " + std::to_string(jbase + J) + ") outside [0, " +
+            std::to_string(n) + ")";
+      rc = SO3_ERR_INVALID;
+    }
+  }
+  if (rc) { close(fd); return fail(rc, why); }
+  const so3io::Rows rw = so3io::slab_rows(kind, h.bandwidth, jbase, J);
+  const long long doubles = (long long)(rw.rows * (long long)rw.row_bytes / 8);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dst_on_device) {
+    rc = so3io::stream_in(fd, rw, static_cast<char*>(dst), (size_t)std::max<int64_t>(staging_bytes, 1 << 20), st, &why);
+    close(fd);
+    if (rc) return fail(rc, std::string(path) + ": " + (why.empty() ? cudaGetErrorString(cudaGetLastError()) : why));
+    unsigned long long bad = 0;
+    if (so3io::device_nonfinite(dst, doubles, st, &bad)) return fail(SO3_ERR_CUDA, "non-finite check failed");
+    if (bad) return fail(SO3_ERR_INVALID, std::string(path) + ": payload contains non-finite values");
+    return SO3_OK;
+  }
+  char* out = static_cast<char*>(dst);
+  bool ok = true;
+  if (rw.file_stride == (off_t)rw.row_bytes) ok = so3io::pread_all(fd, out, (size_t)rw.rows * rw.row_bytes, rw.off0);
+  else
+    for (long long r = 0; ok && r < rw.rows; ++r)
+      ok = so3io::pread_all(fd, out + r * rw.row_bytes, rw.row_bytes, rw.off0 + (off_t)r * rw.file_stride);
+  close(fd);
+  if (!ok) return fail(SO3_ERR_INVALID, std::string(path) + ": read failed");
+  if (so3io::host_nonfinite(reinterpret_cast<const double*>(dst), doubles))
+    return fail(SO3_ERR_INVALID, std::string(path) + ": payload contains non-finite values");
+  return SO3_OK;
+}
+
+int so3_write_container(const char* path, int kind, int bandwidth, int jbase, int J, const void* src, int src_on_device,
+                        int create, int64_t staging_bytes, void* stream) {
+  if (!path || !src) return fail(SO3_ERR_INVALID, "null path or source");
+  if (!valid_bandwidth(bandwidth) || (kind != 0 && kind != 1)) return fail(SO3_ERR_INVALID, "bad bandwidth or kind");
+  const int n = 2 * bandwidth;
+  if (kind == 1) {
+    if (J == 0) { jbase = 0; J = n; }
+    if (jbase < 0 || J < 1 || jbase + J > n) return fail(SO3_ERR_INVALID, "beta slab outside the grid");
+  }
+  const so3io::Rows rw = so3io::slab_rows(kind, bandwidth, jbase, J);
+  const long long doubles = (long long)(rw.rows * (long long)rw.row_bytes / 8);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // the reference refuses to persist non-finite values (core.py:180-181): checked before the file is touched
+  if (src_on_device) {
+    unsigned long long bad = 0;
+    if (so3io::device_nonfinite(src, doubles, st, &bad)) return fail(SO3_ERR_CUDA, "non-finite check failed");
+    if (bad) return fail(SO3_ERR_INVALID, "refusing to persist non-finite values");
+  } else if (so3io::host_nonfinite(static_cast<const double*>(src), doubles)) {
+    return fail(SO3_ERR_INVALID, "refusing to persist non-finite values");
+  }
+  const int fd = open(path, create ? (O_WRONLY | O_CREAT | O_TRUNC) : O_RDWR, 0644);
+  if (fd < 0) return fail(SO3_ERR_INVALID, std::string(path) + ": " + strerror(errno));
+  std::string why;
+  int rc = SO3_OK;
+  if (create) {
+    unsigned char head[so3io::kHeader];
+    memcpy(head, kind ? "SOFG" : "SOFC", 4);
+    const uint32_t v = so3io::kVersion, b = (uint32_t)bandwidth;
+    memcpy(head + 4, &v, 4);
+    memcpy(head + 8, &b, 4);
+    if (!so3io::pwrite_all(fd, head, so3io::kHeader, 0) ||
+        ftruncate(fd, (off_t)so3io::kHeader + (off_t)so3io::expected_elements(kind, bandwidth) * 16) != 0) {
+      why = strerror(errno);
+      rc = SO3_ERR_INVALID;
+    }
+  } else {
+    so3io::Header h;
+    rc = so3io::parse_header(fd, path, &h, &why);
+    if (!rc && (h.kind != kind || h.bandwidth != bandwidth)) {
+      why = std::string(path) + ": existing container does not match (kind, bandwidth)";
+      rc = SO3_ERR_INVALID;
+    }
+  }
+  if (!rc) {
+    if (src_on_device) {
+      rc = so3io::stream_out(fd, rw, static_cast<const char*>(src), (size_t)std::max<int64_t>(staging_bytes, 1 << 20),
+                             st, &why);
+    } else {
+      const char* in = static_cast<const char*>(src);
+      bool ok = true;
+      if (rw.file_stride == (off_t)rw.row_bytes) ok = so3io::pwrite_all(fd, in, (size_t)rw.rows * rw.row_bytes, rw.off0);
+      else
+        for (long long r = 0; ok && r < rw.rows; ++r)
+          ok = so3io::pwrite_all(fd, in + r * rw.row_bytes, rw.row_bytes, rw.off0 + (off_t)r * rw.file_stride);
+      if (!ok) { why = strerror(errno); rc = SO3_ERR_INVALID; }
+    }
+  }
+  close(fd);
+  if (rc) return fail(rc, std::string(path) + ": " + why);
+  return SO3_OK;
 }
 
 static unsigned blocks_for(long long count) { return (unsigned)((count + 255) / 256); }

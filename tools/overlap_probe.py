@@ -16,11 +16,14 @@ import paper_1808_00896_b200 as so3  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("-B", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--pads", type=lambda t: [int(x) for x in t.split(",")], default=[0, 60, 100, 130])
+ap.add_argument("--carveout", type=int, default=-1, help="preferred smem carveout of every big kernel (-1: default)")
 args = ap.parse_args()
 b = args.B
 n = 2 * b
 dev = torch.device("cuda", 0)
 plan = so3.make_plan(b, device=dev)
+plan.set_knob("carveout", args.carveout)
 g = torch.randn(n ** 3, dtype=torch.complex128, device=dev)
 spec_a = torch.randn(n ** 3, dtype=torch.complex128, device=dev)
 spec_b = torch.empty_like(spec_a)
@@ -81,9 +84,14 @@ def pair(first, second, s1, s2):
     return run
 
 
-for tag, (dwt, fft) in {"forward": (fwd_dwt, fwd_fft), "inverse": (inv_dwt, inv_fft)}.items():
-    res[f"{tag}_serial"] = timed(lambda: (dwt(), fft()))
-    res[f"{tag}_dwt_first_fft_hi"] = timed(pair(dwt, fft, lo, hi))
-    res[f"{tag}_fft_first_fft_hi"] = timed(pair(fft, dwt, hi, lo))
-    res[f"{tag}_dwt_first_same_prio"] = timed(pair(dwt, fft, lo, torch.cuda.Stream(device=dev)))
+for pad in args.pads:
+    plan.set_knob("fft_pad", pad)
+    for tag, (dwt, fft) in {"forward": (fwd_dwt, fwd_fft), "inverse": (inv_dwt, inv_fft)}.items():
+        res[f"pad{pad}_{tag}_fft_alone"] = timed(fft)
+        res[f"pad{pad}_{tag}_serial"] = timed(lambda: (dwt(), fft()))
+        res[f"pad{pad}_{tag}_dwt_first_fft_hi"] = timed(pair(dwt, fft, lo, hi))
+        res[f"pad{pad}_{tag}_fft_first_fft_hi"] = timed(pair(fft, dwt, hi, lo))
+        res[f"pad{pad}_{tag}_dwt_first_same_prio"] = timed(pair(dwt, fft, lo, torch.cuda.Stream(device=dev)))
+    print(json.dumps({k: v for k, v in res.items() if k.startswith(f"pad{pad}_")}), flush=True)
+plan.set_knob("fft_pad", 0)
 print(json.dumps(res, indent=1))
