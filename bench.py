@@ -521,17 +521,20 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     def step_staged(evs=None):
         rec = (lambda i: evs[i].record(stream)) if evs is not None else (lambda i: None)
         rec(0)
+        # one rank: layouts A and B coincide, so the exchange is elided (ShardedSO3 does the same)
         backend.dwt_synthesis(coeffs, send_b)
         rec(1)
-        sh._all_to_all(recv_a, send_b, m.inverse_recv_splits(rank), m.inverse_send_splits(rank))
+        if world > 1:
+            sh._all_to_all(recv_a, send_b, m.inverse_recv_splits(rank), m.inverse_send_splits(rank))
         rec(2)
-        backend.fft_synthesis(recv_a, slab)
+        backend.fft_synthesis(recv_a if world > 1 else send_b, slab)
         rec(3)
         backend.fft_analysis(slab, send_a)
         rec(4)
-        sh._all_to_all(recv_b, send_a, m.forward_recv_splits(rank), m.forward_send_splits(rank))
+        if world > 1:
+            sh._all_to_all(recv_b, send_a, m.forward_recv_splits(rank), m.forward_send_splits(rank))
         rec(5)
-        backend.dwt_analysis(recv_b, out)
+        backend.dwt_analysis(recv_b if world > 1 else send_a, out)
         rec(6)
         result["coeffs"] = out
 

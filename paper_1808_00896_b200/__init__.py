@@ -17,14 +17,17 @@ from .core import (
     So3SampleGrid,
     coeff_count,
     coeff_index,
+    container_info,
     degree_of_slots,
     grid_size,
     order_pair_slots,
     read_coefficients,
     read_samples,
+    read_samples_slab,
     validate_bandwidth,
     write_coefficients,
     write_samples,
+    write_samples_slab,
 )
 from .soft import (
     DIRECT_BANDWIDTH_CAP,

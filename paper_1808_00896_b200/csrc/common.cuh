@@ -97,21 +97,30 @@ __device__ __forceinline__ double seed_value(int m, int mp, double2 lnorm, doubl
   return exp(hi) * (1.0 + lo);
 }
 
-// Recurrence coefficients of reference wigner.py:165-174 for the step l -> l+1,
-// stored as (A, A*shift, C) for  d^{l+1} = (A x - A*shift) d^l - C d^{l-1}.
-// All integer products are exact in double (|.| < 2^53 for B < 2^13) and IEEE
-// sqrt/div are correctly rounded, so A, shift and C equal the reference's bit for bit.
+// Recurrence coefficients of reference wigner.py:165-174 for the step l -> l+1, stored as
+// (A, C+, C) with C+ = A (1 - shift) = A (l(l+1) - m m') / (l(l+1)) (integer numerator, so
+// C+ carries no cancellation) for  d^{l+1} = t_l d^l - C d^{l-1},  t_l = A (x - shift).
 __device__ __forceinline__ double3 recurrence_coeffs(int l, int m, int mp) {
   const double lp = (double)(l + 1);
   const double dl = (double)l;
   const double denom = sqrt((lp * lp - (double)m * m) * (lp * lp - (double)mp * mp));
   const double a = (lp * (2.0 * dl + 1.0)) / denom;
-  double shift = 0.0, c = 0.0;
+  double cplus = a, c = 0.0;
   if (l > 0) {
-    shift = ((double)m * (double)mp) / (dl * lp);
+    const double ll1 = dl * lp;   // l(l+1), exact
+    cplus = a * ((ll1 - (double)m * (double)mp) / ll1);
     c = (lp * sqrt((dl * dl - (double)m * m) * (dl * dl - (double)mp * mp))) / (dl * denom);
   }
-  return make_double3(a, a * shift, c);
+  return make_double3(a, cplus, c);
+}
+
+// t_l = A (x - shift) without a rounded cos(beta): the plan stores v_j with x_j = 1 + v_j for
+// beta_j < pi/2 (v = -2 sin^2(beta/2)) and x_j = -1 + v_j above (v = 2 cos^2(beta/2)), both to
+// full relative precision, so t = A v + C+ (lower half) or A v + C+ - 2A (upper half).  Near the
+// poles the reference's rounded cos(beta) moves d^l by l^2/2 ulps (P_l'(1) = l(l+1)/2); this
+// form does not (oracle/extended.py measures it).
+__device__ __forceinline__ double rec_t(double alpha, double cplus, double v, bool upper) {
+  return fma(alpha, v, upper ? fma(-2.0, alpha, cplus) : cplus);
 }
 
 }  // namespace so3

@@ -37,12 +37,12 @@ __host__ __device__ inline int batch_sd(int n) {   // >= np, = 4 (mod 16) when n
 // Wigner tile rows l0 .. l0+31 of the cluster for this thread's j (rows past B-1 are zero);
 // recurrence table entries come through L1 (every thread of the CTA reads the same ones).
 __device__ __forceinline__ void batch_wigner_tile_ldg(double* D, int sd, int t, int nl, const double* rct, int l0m,
-                                                      double x, double& cur, double& prev) {
+                                                      double x, bool up, double& cur, double& prev) {
 #pragma unroll 4
   for (int ll = 0; ll < 32; ++ll) {
     if (ll < nl) {
       D[ll * sd + t] = cur;
-      const double tt = fma(__ldg(&rct[3 * (l0m + ll)]), x, -__ldg(&rct[3 * (l0m + ll) + 1]));
+      const double tt = rec_t(__ldg(&rct[3 * (l0m + ll)]), __ldg(&rct[3 * (l0m + ll) + 1]), x, up);
       const double nx = fma(tt, cur, -prev);
       prev = cur;
       cur = nx;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
   const double* rct = a.rc + 3 * rco;
   double x = 0.0, cur = 0.0, prev = 0.0;
   if (t < n) {
-    x = __ldg(&a.cosb[t]);
+    x = __ldg(&a.xv[t]);
     cur = seed_value(m, mp, ln, a.logcs[t]);
   }
   const bool two_tiles = mem[4].valid;
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
   for (int l0 = m; l0 < B; l0 += 32) {
     const int nl = min(32, B - l0);
     if (l0 > m) __syncthreads();   // every warp is done reading the previous tile
-    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, cur, prev);
+    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, 2 * t >= n, cur, prev);
     __syncthreads();
     if (!fvalid) continue;
     const int mtn = (nl + 7) >> 3;
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs
 
   double x = 0.0, cur = 0.0, prev = 0.0;
   if (t < n) {
-    x = __ldg(&a.cosb[t]);
+    x = __ldg(&a.xv[t]);
     cur = seed_value(m, mp, __ldg(&a.lnorm[c]), a.logcs[t]);
   }
   const bool two_tiles = mem[4].valid;
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs
   for (int l0 = m; l0 < B; l0 += 32) {
     const int nl = min(32, B - l0);
     if (l0 > m) __syncthreads();   // every warp is done reading the previous Wigner tile
-    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, cur, prev);
+    if (t < np) batch_wigner_tile_ldg(D, sd, t, nl, rct, l0 - m, x, 2 * t >= n, cur, prev);
     // this warp's signed, mu-scaled coefficients of the tile (its own previous reads are
     // complete: same warp, program order)
 #pragma unroll

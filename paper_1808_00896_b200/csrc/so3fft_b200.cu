@@ -15,6 +15,10 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <thread>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "../../include/so3fft_b200.h"
 #include "common.cuh"
@@ -49,12 +53,27 @@ constexpr int kMaxBandwidth = 512;   // DWT kernels: at most 2B = 1024 beta indi
 // Carveout, a per-kernel, process-wide attribute; -1 = driver default).  Kernels with different
 // carveouts cannot share an SM, so concurrent FFT and DWT launches need the same one.
 int g_carveout = -1;
+// extra KB of dynamic shared memory per MMA DWT CTA (experiments: fewer DWT CTAs per SM)
+int g_dwt_pad = 0;
 
+// The attributes are set once per (kernel, device, value): cudaFuncSetAttribute on a kernel that
+// may be running is not free, and launches on other streams must not wait behind it.
 template <typename K>
 cudaError_t set_smem(K k, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int>, std::pair<size_t, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(k), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(key);
+  const size_t have = it == done.end() ? 48 * 1024 : it->second.first;
+  const int cv = it == done.end() ? -1 : it->second.second;
   cudaError_t e = cudaSuccess;
-  if (smem > 48 * 1024) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (!e && g_carveout >= 0) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
+  if (smem > have) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (!e && g_carveout != cv && g_carveout >= 0)
+    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
+  if (!e) done[key] = {std::max(have, smem), g_carveout >= 0 ? g_carveout : cv};
   return e;
 }
 
@@ -153,7 +172,7 @@ struct so3_plan_s {
   int64_t ncoef = 0, ngrid = 0, nclusters = 0;
   int2* d_bases = nullptr;
   double2* d_lnorm = nullptr;
-  double* d_cosb = nullptr;
+  double* d_xv = nullptr;            // v_j of rec_t: cos(beta_j) = (j < B ? 1 : -1) + v_j
   double4* d_logcs = nullptr;
   double* d_w = nullptr;
   double2* d_tw = nullptr;
@@ -208,7 +227,7 @@ int launch_fft_pow2(const so3_plan_s* p, const so3::FftArgs& a, int sign, int ba
     constexpr int NT = (N == 256 || N == 512 || N == 1024) ? N : 256;
     auto kt = sign > 0 ? so3::fft_tab_tma_kernel<NT, 4, +1> : so3::fft_tab_tma_kernel<NT, 4, -1>;
     const size_t smem_t = (size_t)4 * so3::RowLayout<NT, 4>::SIZE * sizeof(double2) + 16;
-    if (smem_t > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t));
+    SO3_CUDA(set_smem(kt, smem_t));
     grid.x = (grid.x + p->fft_tab_loop - 1) / p->fft_tab_loop;
     kt<<<grid, threads, smem_t, st>>>(a);
     SO3_CUDA(cudaGetLastError());
@@ -216,7 +235,7 @@ int launch_fft_pow2(const so3_plan_s* p, const so3::FftArgs& a, int sign, int ba
   }
   if (tab && p->fft_tab_loop > 0) {
     auto kt = sign > 0 ? so3::fft_tab_kernel<N, XB, +1> : so3::fft_tab_kernel<N, XB, -1>;
-    if (smem > 48 * 1024) SO3_CUDA(cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SO3_CUDA(set_smem(kt, smem));
     grid.x = (grid.x + p->fft_tab_loop - 1) / p->fft_tab_loop;
     kt<<<grid, threads, smem, st>>>(a);
     SO3_CUDA(cudaGetLastError());
@@ -503,11 +522,15 @@ int dwt_jw(int n) {
   return 32;
 }
 
+// Warps straddle beta = pi/2 (rec_t's two table halves) unless B is a multiple of JW.
+inline bool straddles(const so3::DwtArgs& a, int jw) { return a.B % jw != 0; }
+
 template <int JW, int WPC, int FG = 1>
 int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
-  const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double);
-  auto k = so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG>;
+  const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double) + (size_t)g_dwt_pad * 1024;
+  auto k = straddles(a, JW) ? so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG, true>
+                            : so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG, false>;
   SO3_CUDA(set_smem(k, smem));
   k<<<dim3(ncl * split, batch / FG), WPC * 32, smem, st>>>(a, split);
   SO3_CUDA(cudaGetLastError());
@@ -519,7 +542,8 @@ int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cu
   using SM = so3::MmaSmem<JW>;
   const int warps = (n + JW - 1) / JW;
   const size_t smem = ((size_t)warps * 8 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
-  auto k = so3::dwt_analysis_mma_cta_kernel<JW, FG>;
+  auto k = straddles(a, JW) ? so3::dwt_analysis_mma_cta_kernel<JW, FG, 8, 1, true>
+                            : so3::dwt_analysis_mma_cta_kernel<JW, FG, 8, 1, false>;
   SO3_CUDA(set_smem(k, smem));
   k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a, so3::SplitArgs{nullptr, 0, nullptr});
   SO3_CUDA(cudaGetLastError());
@@ -572,7 +596,7 @@ int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cuda
   constexpr int JW = 128;
   const int W = p->n / JW / 2;   // warps per half
   using SM = so3::MmaSmem<JW>;
-  const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double);
+  const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double) + (size_t)g_dwt_pad * 1024;
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
   SO3_CUDA(set_smem(k, smem));
   k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a, sp);
@@ -592,7 +616,7 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   a.n = p->n;
   a.bases = p->d_bases;
   a.lnorm = p->d_lnorm;
-  a.cosb = p->d_cosb;
+  a.xv = p->d_xv;
   a.logcs = p->d_logcs;
   a.spec = static_cast<const double2*>(spec);
   a.coef = static_cast<double2*>(coef);
@@ -639,10 +663,11 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
 
 // Rows of d^l_{m,m'} for any pair: base recurrence + relation (sign, reflection).
 __global__ void wigner_rows_kernel(int B, int n, int m, int mp, int bm, int bmp, int reflect, int sl, int par0,
-                                   double2 lnorm, const double* cosb, const double4* logcs, double* out) {
+                                   double2 lnorm, const double* xv, const double4* logcs, double* out) {
   const int L = bm;
   for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double x = cosb[j];
+    const double x = xv[j];
+    const bool up = 2 * j >= n;
     double cur = so3::seed_value(bm, bmp, lnorm, logcs[j]);
     double prev = 0.0;
     const int jo = reflect ? n - 1 - j : j;
@@ -651,7 +676,7 @@ __global__ void wigner_rows_kernel(int B, int n, int m, int mp, int bm, int bmp,
       out[(long long)(l - L) * n + jo] = s * cur;
       if (l < B - 1) {
         const double3 k3 = so3::recurrence_coeffs(l, bm, bmp);
-        const double tt = fma(k3.x, x, -k3.y);
+        const double tt = so3::rec_t(k3.x, k3.y, x, up);
         const double nx = fma(tt, cur, -k3.z * prev);
         prev = cur;
         cur = nx;
@@ -737,16 +762,62 @@ int ensure_split_scratch(so3_plan_s* p) {
   return SO3_OK;
 }
 
+// The rescaled recurrence table, per (cluster, degree l = m..B-1): (alpha_l, C+_l, mu_l) with
+// d^l = mu_l e^l, e^{l+1} = t_l e^l - e^{l-1}, t_l = alpha_l (x - shift_l) (rec_t), mu_m = 1,
+// mu_{l+1} = c_l mu_{l-1} (a_m mu_m at l = m), alpha_l = a_l mu_l / mu_{l+1}, C+_l = alpha_l (1 -
+// shift_l), from the reference's coefficients (wigner.py:165-174).  Evaluated in long double
+// (64-bit mantissa) and rounded once per entry, so mu_l carries no fp64 drift along l; split over
+// the host's cores (67 M entries at B = 512).
+std::vector<double> host_rc_table(int b, const std::vector<Cluster>& cl, const std::vector<long long>& off,
+                                  size_t entries) {
+  std::vector<double> rc(3 * std::max<size_t>(entries, 1), 0.0);
+  const unsigned nt = std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (size_t i = t; i < cl.size(); i += nt) {
+        const long double m = cl[i].m, mp = cl[i].mp;
+        double* dst = rc.data() + 3 * off[i];
+        long double mu_prev = 0.0L, mu = 1.0L;
+        for (int l = cl[i].m; l < b; ++l) {
+          long double alpha = 0.0L, cplus = 0.0L, mu_next = 0.0L;
+          if (l < b - 1) {
+            const long double lp = l + 1.0L, dl = l;
+            const long double denom = sqrtl((lp * lp - m * m) * (lp * lp - mp * mp));
+            const long double a = lp * (2.0L * dl + 1.0L) / denom;
+            long double c = 0.0L, one_minus_shift = 1.0L;
+            if (l > 0) {
+              c = lp * sqrtl((dl * dl - m * m) * (dl * dl - mp * mp)) / (dl * denom);
+              one_minus_shift = (dl * lp - m * mp) / (dl * lp);
+            }
+            mu_next = l == cl[i].m ? a * mu : c * mu_prev;
+            alpha = a * mu / mu_next;
+            cplus = alpha * one_minus_shift;
+          }
+          dst[3 * (l - cl[i].m)] = (double)alpha;
+          dst[3 * (l - cl[i].m) + 1] = (double)cplus;
+          dst[3 * (l - cl[i].m) + 2] = (double)mu;
+          mu_prev = mu;
+          mu = mu_next;
+        }
+      }
+    });
+  for (auto& x : th) x.join();
+  return rc;
+}
+
 // Tables and buffers of a plan over the cluster list `cl` (all clusters, or one rank's group).
 int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   const int b = p->B, n = p->n, batch = p->batch;
-  std::vector<double> w(n), cosb(n);
+  std::vector<double> w(n), xv(n);
   std::vector<double4> logcs(n);
   std::vector<double2> tw(n);
   host_weights(b, w.data());
   for (int j = 0; j < n; ++j) {
     const long double beta = (2.0L * j + 1.0L) * kPi / (4.0L * b);
-    cosb[j] = (double)cosl(beta);
+    // rec_t's v_j: cos(beta) - 1 = -2 sin^2(beta/2) below pi/2, cos(beta) + 1 = 2 cos^2(beta/2) above
+    const long double sh = sinl(0.5L * beta), ch = cosl(0.5L * beta);
+    xv[j] = 2 * j < n ? (double)(-2.0L * sh * sh) : (double)(2.0L * ch * ch);
     double a0, a1, a2, a3;
     split_ld(logl(cosl(0.5L * beta)), &a0, &a1);
     split_ld(logl(sinl(0.5L * beta)), &a2, &a3);
@@ -791,7 +862,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   } while (0)
   PLAN_ALLOC(p->d_bases, ncl);
   PLAN_ALLOC(p->d_lnorm, ncl);
-  PLAN_ALLOC(p->d_cosb, n);
+  PLAN_ALLOC(p->d_xv, n);
   PLAN_ALLOC(p->d_logcs, n);
   PLAN_ALLOC(p->d_w, n);
   PLAN_ALLOC(p->d_tw, n);
@@ -803,14 +874,14 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   cudaError_t e = cudaSuccess;
   e = e ? e : cudaMemcpy(p->d_bases, bases.data(), ncl * sizeof(int2), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_lnorm, lnorm.data(), ncl * sizeof(double2), cudaMemcpyHostToDevice);
-  e = e ? e : cudaMemcpy(p->d_cosb, cosb.data(), n * sizeof(double), cudaMemcpyHostToDevice);
+  e = e ? e : cudaMemcpy(p->d_xv, xv.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_logcs, logcs.data(), n * sizeof(double4), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_w, w.data(), n * sizeof(double), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_tw, tw.data(), n * sizeof(double2), cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpy(p->d_rc_off, rc_off.data(), ncl * sizeof(long long), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !cl.empty()) {
-    so3::rc_table_kernel<<<(unsigned)((cl.size() + 127) / 128), 128>>>(b, (int)cl.size(), p->d_bases, p->d_rc_off, p->d_rc);
-    e = cudaGetLastError();
+    const std::vector<double> rc = host_rc_table(b, cl, rc_off, (size_t)rc_entries);
+    e = cudaMemcpy(p->d_rc, rc.data(), rc.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   e = e ? e : cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
@@ -972,7 +1043,7 @@ void so3_plan_destroy(so3_plan_t p) {
   if (!p) return;
   cudaFree(p->d_bases);
   cudaFree(p->d_lnorm);
-  cudaFree(p->d_cosb);
+  cudaFree(p->d_xv);
   cudaFree(p->d_logcs);
   cudaFree(p->d_w);
   cudaFree(p->d_tw);
@@ -1019,6 +1090,11 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "carveout") {   // process-wide kernel attribute (see g_carveout)
     if (value < -1 || value > 100) return fail(SO3_ERR_INVALID, "carveout must be -1 or a percentage in [0, 100]");
     g_carveout = value;
+    return SO3_OK;
+  }
+  if (k == "dwt_pad") {   // process-wide (see g_dwt_pad)
+    if (value < 0 || value > 150) return fail(SO3_ERR_INVALID, "dwt_pad must be in [0, 150] KB");
+    g_dwt_pad = value;
     return SO3_OK;
   }
   if (k == "fft_pad") {
@@ -1274,11 +1350,7 @@ int so3_read_container(const char* path, int kind, int jbase, int J, void* dst, 
   if (fd < 0) return fail(SO3_ERR_INVALID, std::string(path) + ": " + strerror(errno));
   so3io::Header h;
   std::string why;
-  int rc = so3io::parse_header(fd, path, &h, &why);
-  if (!rc && h.kind != kind) {
-    why = std::string(path) + ": not a " + (kind ? "SOFG" : "SOFC") + " container";
-    rc = SO3_ERR_INVALID;
-  }
+  int rc = so3io::parse_header(fd, path, &h, &why, kind);
   const int n = 2 * h.bandwidth;
   if (!rc && kind == 1) {
     if (J == 0) { jbase = 0; J = n; }
@@ -1438,7 +1510,7 @@ int so3_wigner_rows(so3_plan_t p, int m, int mp, double* out, void* stream) {
   split_ld(ln, &hi, &lo);
   const int par0 = (rel[tag][2] * bm + rel[tag][3] * bmp) & 1;
   wigner_rows_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      p->B, p->n, m, mp, bm, bmp, rel[tag][0], rel[tag][1], par0, make_double2(hi, lo), p->d_cosb, p->d_logcs, out);
+      p->B, p->n, m, mp, bm, bmp, rel[tag][0], rel[tag][1], par0, make_double2(hi, lo), p->d_xv, p->d_logcs, out);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }

@@ -37,13 +37,15 @@ inline int64_t expected_elements(int kind, int b) {
 }
 
 // 0 on success; otherwise an SO3_ERR_* code with the message in *why
-inline int parse_header(int fd, const char* path, Header* h, std::string* why) {
+// want: 0 = SOFC, 1 = SOFG, -1 = either (messages as the reference's core.py:190-198)
+inline int parse_header(int fd, const char* path, Header* h, std::string* why, int want = -1) {
   unsigned char buf[kHeader];
   const ssize_t got = pread(fd, buf, kHeader, 0);
   struct stat st;
   if (fstat(fd, &st) != 0) { *why = std::string(path) + ": " + strerror(errno); return SO3_ERR_INVALID; }
-  if (got != kHeader || (memcmp(buf, "SOFC", 4) != 0 && memcmp(buf, "SOFG", 4) != 0)) {
-    *why = std::string(path) + ": not an SOFC/SOFG container";
+  const bool sofc = got == kHeader && memcmp(buf, "SOFC", 4) == 0, sofg = got == kHeader && memcmp(buf, "SOFG", 4) == 0;
+  if ((want == 0 && !sofc) || (want == 1 && !sofg) || (!sofc && !sofg)) {
+    *why = std::string(path) + ": not a " + (want == 0 ? "SOFC" : want == 1 ? "SOFG" : "SOFC/SOFG") + " container";
     return SO3_ERR_INVALID;
   }
   uint32_t version, b;

@@ -221,6 +221,13 @@ class ShardedSO3:
         m, r = self.map, self.rank
         send = self.backend.empty(m.layout_a_rows() * m.J)
         self.backend.fft_analysis(slab, send)
+        if self.world == 1:
+            # one rank: layouts A and B coincide (every block is the rank's own), no exchange
+            coeffs = self.backend.zeros(self.coeff_count) if out is None else out
+            for q in range(self.chunks):
+                b0, b1 = m.chunk_b(r, q)
+                self.backend.dwt_analysis_chunk(q, send[b0:b1], coeffs)
+            return coeffs
         recv = self.backend.empty(m.layout_b_rows(r) * m.J)
         works = []
         for q in range(self.chunks):
@@ -241,6 +248,13 @@ class ShardedSO3:
         Chunk q is exchanged while chunk q+1 is synthesised."""
         m, r = self.map, self.rank
         send = self.backend.empty(m.layout_b_rows(r) * m.J)
+        if self.world == 1:   # layouts A and B coincide: the DWT output is the FFT input
+            for q in range(self.chunks):
+                b0, b1 = m.chunk_b(r, q)
+                self.backend.dwt_synthesis_chunk(q, coeffs, send[b0:b1])
+            slab = self.backend.empty(self.slab_count)
+            self.backend.fft_synthesis(send, slab)
+            return slab
         recv = self.backend.empty(m.layout_a_rows() * m.J)
         works = []
         for q in range(self.chunks):

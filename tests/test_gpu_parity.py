@@ -168,11 +168,21 @@ def test_sampled_inverse_oracle_at_b512():
     so3.dwt_synthesis(plan, cd, spec)
     sv = spec.view(n, n, n)                          # stored [m'][m][j]
     betas = O.beta_nodes(b)
+    from oracle import extended as E
     for (bm, bmp) in [(0, 0), (7, 0), (300, 300), (400, 123), (511, 510)]:
         rows = O.recurrence_rows(bm, bmp, betas, b)
+        truth = {(m, mp): col for (m, mp, col) in E.synthesis_cluster_ld(b, bm, bmp, c)}
         for (m, mp, tag) in O.cluster_members(bm, bmp):
+            got = sv[mp % n, m % n, :].cpu().numpy()
             ref = O.synthesis_column(O.member_matrix(rows, tag, bm, bmp, b), c[O.pair_slots(m, mp, b)])
-            assert rel_of_max(sv[mp % n, m % n, :].cpu().numpy(), ref) < 1e-12, (m, mp)
+            # against the reference arithmetic: its own fp64 error near the poles (rounded
+            # cos(beta) in the recurrence) is up to ~2.5e-12 of max here; the GPU recurrence
+            # does not round cos(beta) (common.cuh rec_t) and sits 10x closer to the
+            # long-double values
+            assert rel_of_max(got, ref) < 1e-11, (m, mp)
+            tr = truth[(m, mp)].astype(np.complex128)
+            assert rel_of_max(got, tr) < 1e-12, (m, mp)
+            assert np.abs(got - tr).max() <= np.abs(ref - tr).max() * 1.5 + 1e-14, (m, mp)
     del cd
     grid = torch.empty_like(spec)
     so3.fft_synthesis(plan, spec, grid)
@@ -669,3 +679,45 @@ def test_report_harness_device_columns_and_oracles(tmp_path):
     import json
     rows = json.loads(p.read_text())
     assert set(R.EXTENDED_FIELDS) <= set(rows[0]) and rows[0]["dwt_ms"] > 0
+
+
+# ---------------------------------------------------------------- streamed SOFC / SOFG (csrc/sofio.cuh)
+
+def test_streamed_containers_device_side(tmp_path, golden):
+    """Device reads / writes of the reference's container bytes (files written by the reference
+    itself, oracle/gen_sof_golden.py), per-rank beta slabs, and a B=64 iFSOFT grid through a
+    file and back bit-exactly, with staging much smaller than the payload."""
+    import os
+    from paper_1808_00896_b200 import core
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    host = so3.read_samples(os.path.join(gold, "ref_b4.sofg")).data
+    dev = so3.read_samples(os.path.join(gold, "ref_b4.sofg"), device="cuda")
+    assert dev.data.is_cuda and np.array_equal(dev.data.cpu().numpy(), host)
+    so3.write_samples(str(tmp_path / "d.sofg"), dev)
+    assert (tmp_path / "d.sofg").read_bytes() == open(os.path.join(gold, "ref_b4.sofg"), "rb").read()
+    c = so3.read_coefficients(os.path.join(gold, "ref_b4.sofc"), device="cuda")
+    so3.write_coefficients(str(tmp_path / "d.sofc"), c)
+    assert (tmp_path / "d.sofc").read_bytes() == open(os.path.join(gold, "ref_b4.sofc"), "rb").read()
+    b, n = 64, 128
+    plan = plan_for(b)
+    rng = np.random.default_rng(64)
+    coef = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    grid = so3.ifsoft_sequential(so3.So3Coefficients(b, coef), plan)
+    old = core.STAGING_BYTES
+    core.STAGING_BYTES = 1 << 20            # 1 MiB bounce buffers for a 33.5 MB grid
+    try:
+        so3.write_samples(str(tmp_path / "g.sofg"), grid)
+        back = so3.read_samples(str(tmp_path / "g.sofg"), device="cuda")
+        assert torch.equal(back.data, grid.data)
+        J = n // 4
+        for r in range(4):
+            sl = so3.read_samples_slab(str(tmp_path / "g.sofg"), r * J, J, device="cuda")
+            assert torch.equal(sl.view(n, J, n), grid.data.view(n, n, n)[:, r * J:(r + 1) * J, :])
+            so3.write_samples_slab(str(tmp_path / "s.sofg"), b, sl, r * J, J, create=(r == 0))
+        assert (tmp_path / "s.sofg").read_bytes() == (tmp_path / "g.sofg").read_bytes()
+    finally:
+        core.STAGING_BYTES = old
+    bad = grid.data.clone()
+    bad[12345] = complex(float("nan"), 0.0)
+    with pytest.raises(ValueError, match="non-finite"):
+        so3.write_samples(str(tmp_path / "bad.sofg"), so3.So3SampleGrid(b, bad))

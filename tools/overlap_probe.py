@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("-B", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--pads", type=lambda t: [int(x) for x in t.split(",")], default=[0, 60, 100, 130])
+ap.add_argument("--dwt-pads", type=lambda t: [int(x) for x in t.split(",")], default=[])
 ap.add_argument("--carveout", type=int, default=-1, help="preferred smem carveout of every big kernel (-1: default)")
 args = ap.parse_args()
 b = args.B
@@ -60,6 +61,11 @@ fwd_fft = lambda: so3.fft_analysis(plan, g, spec_b)
 fwd_dwt = lambda: so3.dwt_analysis(plan, spec_a, coef)
 inv_dwt = lambda: so3.dwt_synthesis(plan, coef, spec_b)
 inv_fft = lambda: so3.fft_synthesis(plan, spec_a, grid2)
+for dpad in args.dwt_pads:
+    plan.set_knob("dwt_pad", dpad)
+    res[f"dwt_pad{dpad}_analysis"] = timed(fwd_dwt)
+    res[f"dwt_pad{dpad}_synthesis"] = timed(inv_dwt)
+plan.set_knob("dwt_pad", 0)
 for name, f in (("fft_analysis", fwd_fft), ("dwt_analysis", fwd_dwt), ("dwt_synthesis", inv_dwt),
                 ("fft_synthesis", inv_fft)):
     res[name] = timed(f)
