@@ -368,4 +368,152 @@ __global__ void __launch_bounds__(XB * N / 16, (XB * N / 16 <= 128 ? 3 : XB * N 
   }
 }
 
+// ---------------------------------------------------------------- persistent (co-resident) passes
+// The same passes as one persistent CTA per slot (grid = the number of CTAs the caller lets the
+// FFT occupy, e.g. one per SM beside DWT CTAs), walking tiles t = blockIdx.x + k * gridDim.x with
+// two shared-memory stages: the next tile's row loads (rows in) or tensor load (chunks in) are in
+// flight while this tile is transformed.  Radix code and order are the per-tile kernels', so the
+// results are bit-identical.  Tiles index (xt, y', f) with the skipped row y = skip_y removed.
+struct TileSpace {
+  int nxt, ny, skip;
+  __device__ __forceinline__ void decode(long long tile, int& xt, int& y, int& f) const {
+    xt = (int)(tile % nxt);
+    const long long r = tile / nxt;
+    const int yy = (int)(r % ny);
+    f = (int)(r / ny);
+    y = (skip >= 0 && yy >= skip) ? yy + 1 : yy;
+  }
+};
+
+template <int N, int XB, int SIGN>
+__global__ void __launch_bounds__(XB * N / 16, 2)
+    fft_pass_tstore_persist_kernel(const __grid_constant__ CUtensorMap omap, FftArgs a, TileSpace ts, long long ntiles) {
+  extern __shared__ __align__(1024) double2 smem[];
+  constexpr int TPR = N / 16, SIZE = RowLayout<N, XB>::SIZE, STAGE = XB * SIZE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  const int tid = threadIdx.x, xl = tid % XB, t = tid / XB;
+  auto issue = [&](long long tile, int s) {   // thread 0: the tile's XB rows into stage s
+    int xt, y, f;
+    ts.decode(tile, xt, y, f);
+    mbar_expect_tx(&bar[s], XB * N * sizeof(double2));
+    const double2* r0 = a.src + (long long)f * a.fs_in + (long long)y * a.sy_in + (long long)xt * XB * a.sx_in;
+#pragma unroll
+    for (int r = 0; r < XB; ++r)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_addr(smem + s * STAGE + r * SIZE)),
+                   "l"(r0 + r * a.sx_in), "r"((uint32_t)(N * sizeof(double2))), "r"(smem_addr(&bar[s]))
+                   : "memory");
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    double2* st = smem + s * STAGE;
+    double2* row = st + xl * SIZE;
+    if (tid == 0 && tile + gridDim.x < ntiles) {
+      // stage s^1 was last read by the previous tile's tensor store
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + gridDim.x, s ^ 1);
+    }
+    int xt, y, f;
+    ts.decode(tile, xt, y, f);
+    while (!mbar_try_wait(&bar[s], (it >> 1) & 1)) {
+    }
+    double2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : row[p];
+    }
+    __syncthreads();   // the rows are in registers before the exchange reuses them
+    fft_rows<N, SIGN>(v, t, a.tw, row);   // ends behind a barrier
+    const int x = xt * XB + xl;
+    const double wx = a.weight ? __ldg(&a.w[a.jbase + x]) : 1.0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) st[(t + e * TPR) * XB + xl] = make_double2(v[e].x * wx, v[e].y * wx);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      tensor_store5(&omap, 2 * xt * XB, 0, 0, y, f, st);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+template <int N, int XB, int SIGN, bool BULKOUT>
+__global__ void __launch_bounds__(XB * N / 16, 2)
+    fft_pass_tload_persist_kernel(const __grid_constant__ CUtensorMap imap, FftArgs a, TileSpace ts, long long ntiles) {
+  extern __shared__ __align__(1024) double2 smem[];
+  constexpr int TPR = N / 16, SIZE = RowLayout<N, XB>::SIZE, STAGE = XB * SIZE;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  const int tid = threadIdx.x, xl = tid % XB, t = tid / XB;
+  auto issue = [&](long long tile, int s) {   // thread 0: the tile's chunk side into stage s
+    int xt, y, f;
+    ts.decode(tile, xt, y, f);
+    mbar_expect_tx(&bar[s], XB * N * sizeof(double2));
+    tensor_load5(smem + s * STAGE, &imap, 2 * xt * XB, 0, 0, y, f, &bar[s]);
+  };
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if ((long long)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  int it = 0;
+  for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int s = it & 1;
+    double2* st = smem + s * STAGE;
+    if (tid == 0 && tile + gridDim.x < ntiles) {
+      if constexpr (BULKOUT) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier generic use of stage s^1
+      issue(tile + gridDim.x, s ^ 1);
+    }
+    int xt, y, f;
+    ts.decode(tile, xt, y, f);
+    while (!mbar_try_wait(&bar[s], (it >> 1) & 1)) {
+    }
+    double2 v[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int p = t + e * TPR;
+      v[e] = p == a.zero_p ? make_double2(0.0, 0.0) : st[p * XB + xl];
+    }
+    __syncthreads();   // the box is in registers before the rows are reused for the exchange
+    double2* row = st + xl * SIZE;
+    fft_rows<N, SIGN>(v, t, a.tw, row);
+    if constexpr (BULKOUT) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) row[t + e * TPR] = v[e];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        double2* d0 = a.dst + (long long)f * a.fs_out + (long long)y * a.sy_out + (long long)xt * XB * a.sx_out;
+#pragma unroll
+        for (int r = 0; r < XB; ++r)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(d0 + r * a.sx_out),
+                       "r"(smem_addr(st + r * SIZE)), "r"((uint32_t)(N * sizeof(double2)))
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    } else {
+      double2* dst = a.dst + (long long)f * a.fs_out + (long long)y * a.sy_out + (long long)(xt * XB + xl) * a.sx_out;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) dst[t + e * TPR] = v[e];
+      __syncthreads();   // every thread is done with stage s before it is reloaded
+    }
+  }
+  if constexpr (BULKOUT) {
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  }
+}
+
 }  // namespace so3

@@ -209,6 +209,7 @@ struct so3_plan_s {
   int fft_tab_tma = 1;   // row-table passes move their plain-strided side by bulk copies
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
   int fft_pad = 0;    // extra KB of shared memory per TMA FFT pass CTA (limits FFT CTAs per SM when co-running)
+  int fft_persist = 0;  // > 0: TMA passes as this many persistent double-buffered CTAs (fft_tma.cuh)
 };
 
 // ------------------------------------------------------------------ launches
@@ -410,10 +411,78 @@ int launch_fft_tload_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, cu
   return SO3_OK;
 }
 
+// Persistent variants (fft_tma.cuh): `ctas` CTAs walk all tiles, two smem stages each.
+template <int N, int SIGN>
+int launch_fft_tstore_persist_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, int ctas, cudaStream_t st) {
+  constexpr int XB = 4;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  const int plo = N < 256 ? N : 256, phi = N / plo;
+  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_out * 16, (cuuint64_t)plo * a.sp_out * 16, (cuuint64_t)a.sy_out * 16,
+                                 (cuuint64_t)std::max<long long>(a.fs_out, 1) * 16};
+  const cuuint32_t box[5] = {(cuuint32_t)(2 * XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, a.dst, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const so3::TileSpace ts{a.X / XB, a.Y - ((a.skip_y >= 0 && a.skip_y < a.Y) ? 1 : 0), a.skip_y};
+  const long long ntiles = (long long)ts.nxt * ts.ny * batch;
+  const size_t smem = 2 * (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  auto k = so3::fft_pass_tstore_persist_kernel<N, XB, SIGN>;
+  SO3_CUDA(set_smem(k, smem));
+  k<<<(unsigned)std::min<long long>(ctas, ntiles), XB * N / 16, smem, st>>>(map, a, ts, ntiles);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+template <int N, int SIGN>
+int launch_fft_tload_persist_t(const so3_plan_s* p, const so3::FftArgs& a, int batch, int ctas, cudaStream_t st) {
+  constexpr int XB = 4;
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return -1;
+  const int plo = N < 256 ? N : 256, phi = N / plo;
+  const cuuint64_t dims[5] = {(cuuint64_t)2 * a.X, (cuuint64_t)plo, (cuuint64_t)phi, (cuuint64_t)a.Y, (cuuint64_t)batch};
+  const cuuint64_t strides[4] = {(cuuint64_t)a.sp_in * 16, (cuuint64_t)plo * a.sp_in * 16, (cuuint64_t)a.sy_in * 16,
+                                 (cuuint64_t)std::max<long long>(a.fs_in, 1) * 16};
+  const cuuint32_t box[5] = {(cuuint32_t)(2 * XB), (cuuint32_t)plo, (cuuint32_t)phi, 1, 1};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUtensorMap map;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(a.src), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  const so3::TileSpace ts{a.X / XB, a.Y - ((a.skip_y >= 0 && a.skip_y < a.Y) ? 1 : 0), a.skip_y};
+  const long long ntiles = (long long)ts.nxt * ts.ny * batch;
+  const size_t smem = 2 * (size_t)XB * so3::RowLayout<N, XB>::SIZE * sizeof(double2) + 16;
+  const bool bulkout = p->fft_bulkout < 0 ? N >= 512 : p->fft_bulkout != 0;
+  auto k = bulkout ? so3::fft_pass_tload_persist_kernel<N, XB, SIGN, true> : so3::fft_pass_tload_persist_kernel<N, XB, SIGN, false>;
+  SO3_CUDA(set_smem(k, smem));
+  k<<<(unsigned)std::min<long long>(ctas, ntiles), XB * N / 16, smem, st>>>(map, a, ts, ntiles);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 int launch_fft_tma(const so3_plan_s* p, const so3::FftArgs& a, int sign, cudaStream_t st) {
   // plain-stride passes at 2B in {256, 512, 1024}: rows-in -> TMA chunk stores, chunks-in -> TMA chunk loads
   if (!p->fft_tma || p->fft_wide || a.tab_in || a.tab_out || a.X % 4) return -1;
   if (a.n != 256 && a.n != 512 && a.n != 1024) return -1;
+  const int pc = p->fft_persist;
+  if (pc > 0 && a.sp_in == 1 && a.sx_out == 1) {
+    switch (a.n) {
+      case 256: return sign > 0 ? launch_fft_tstore_persist_t<256, +1>(p, a, p->batch, pc, st) : launch_fft_tstore_persist_t<256, -1>(p, a, p->batch, pc, st);
+      case 512: return sign > 0 ? launch_fft_tstore_persist_t<512, +1>(p, a, p->batch, pc, st) : launch_fft_tstore_persist_t<512, -1>(p, a, p->batch, pc, st);
+      default: return sign > 0 ? launch_fft_tstore_persist_t<1024, +1>(p, a, p->batch, pc, st) : launch_fft_tstore_persist_t<1024, -1>(p, a, p->batch, pc, st);
+    }
+  }
+  if (pc > 0 && a.sp_in != 1 && a.sx_in == 1 && a.sp_out == 1 && !a.weight) {
+    switch (a.n) {
+      case 256: return sign > 0 ? launch_fft_tload_persist_t<256, +1>(p, a, p->batch, pc, st) : launch_fft_tload_persist_t<256, -1>(p, a, p->batch, pc, st);
+      case 512: return sign > 0 ? launch_fft_tload_persist_t<512, +1>(p, a, p->batch, pc, st) : launch_fft_tload_persist_t<512, -1>(p, a, p->batch, pc, st);
+      default: return sign > 0 ? launch_fft_tload_persist_t<1024, +1>(p, a, p->batch, pc, st) : launch_fft_tload_persist_t<1024, -1>(p, a, p->batch, pc, st);
+    }
+  }
   if (a.sp_in == 1 && a.sx_out == 1) {
     switch (a.n) {
       case 256: return sign > 0 ? launch_fft_tstore_t<256, +1>(p, a, p->batch, st) : launch_fft_tstore_t<256, -1>(p, a, p->batch, st);
@@ -536,6 +605,7 @@ int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
+
 
 template <int JW, int FG = 1>
 int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
@@ -1095,6 +1165,11 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "dwt_pad") {   // process-wide (see g_dwt_pad)
     if (value < 0 || value > 150) return fail(SO3_ERR_INVALID, "dwt_pad must be in [0, 150] KB");
     g_dwt_pad = value;
+    return SO3_OK;
+  }
+  if (k == "fft_persist") {
+    if (value < 0 || value > 65536) return fail(SO3_ERR_INVALID, "fft_persist must be in [0, 65536] CTAs");
+    p->fft_persist = value;
     return SO3_OK;
   }
   if (k == "fft_pad") {

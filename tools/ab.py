@@ -23,7 +23,7 @@ stages = {
     "dwt_analysis": lambda: so3.dwt_analysis(plan, spec, out),
 }
 res = {i: {s: [] for s in stages} for i in range(len(configs))}
-defaults = {"dwt_variant": 0, "syn_jw": 0, "ana_split": 1, "fft_xb": 0, "dwt_batch": 1, "fft_fused": 1, "fft_tma": 1, "fft_bulkin": 1, "fft_bulkout": -1}
+defaults = { "dwt_variant": 0, "syn_jw": 0, "ana_split": 1, "fft_xb": 0, "dwt_batch": 1, "fft_fused": 1, "fft_tma": 1, "fft_bulkin": 1, "fft_bulkout": -1}
 for rep in range(int(os.environ.get("AB_REPS", "7"))):
     for i, cfg in enumerate(configs):
         for k, v in defaults.items():

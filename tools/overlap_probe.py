@@ -18,6 +18,7 @@ ap.add_argument("-B", type=int, default=512)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--pads", type=lambda t: [int(x) for x in t.split(",")], default=[0, 60, 100, 130])
 ap.add_argument("--dwt-pads", type=lambda t: [int(x) for x in t.split(",")], default=[])
+ap.add_argument("--persist", type=lambda t: [int(x) for x in t.split(",")], default=[])
 ap.add_argument("--carveout", type=int, default=-1, help="preferred smem carveout of every big kernel (-1: default)")
 args = ap.parse_args()
 b = args.B
@@ -100,4 +101,21 @@ for pad in args.pads:
         res[f"pad{pad}_{tag}_dwt_first_same_prio"] = timed(pair(dwt, fft, lo, torch.cuda.Stream(device=dev)))
     print(json.dumps({k: v for k, v in res.items() if k.startswith(f"pad{pad}_")}), flush=True)
 plan.set_knob("fft_pad", 0)
+ref_fwd = torch.empty_like(spec_b)
+so3.fft_analysis(plan, g, ref_fwd)
+ref_inv = torch.empty_like(grid2)
+so3.fft_synthesis(plan, spec_a, ref_inv)
+for pc in args.persist:
+    plan.set_knob("fft_persist", pc)
+    so3.fft_analysis(plan, g, spec_b)
+    so3.fft_synthesis(plan, spec_a, grid2)
+    torch.cuda.synchronize()
+    res[f"persist{pc}_bit_identical"] = bool(torch.equal(spec_b, ref_fwd)) and bool(torch.equal(grid2, ref_inv))
+    for tag, (dwt, fft) in {"forward": (fwd_dwt, fwd_fft), "inverse": (inv_dwt, inv_fft)}.items():
+        res[f"persist{pc}_{tag}_fft_alone"] = timed(fft)
+        res[f"persist{pc}_{tag}_serial"] = timed(lambda: (dwt(), fft()))
+        res[f"persist{pc}_{tag}_fft_first_fft_hi"] = timed(pair(fft, dwt, hi, lo))
+        res[f"persist{pc}_{tag}_fft_first_same"] = timed(pair(fft, dwt, lo, torch.cuda.Stream(device=dev)))
+    print(json.dumps({k: v for k, v in res.items() if k.startswith(f"persist{pc}_")}), flush=True)
+plan.set_knob("fft_persist", 0)
 print(json.dumps(res, indent=1))
