@@ -209,6 +209,29 @@ class ReferenceSample:
         return t
 
 
+def committed_parity(b: int) -> dict:
+    """Per-direction parity of this bandwidth against the reference arithmetic, measured by
+    tools/parity_full.py (oracle/parity.py) and committed under profiles/; summarised here so the
+    bench line carries it (the bench does not re-run the 4-minute oracle)."""
+    path = os.path.join(ROOT, "profiles", f"r02_parity_B{b}.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as fh:
+        r = json.load(fh)
+    truth = lambda k: {"gpu_err": r[k]["truth"]["gpu_max_err"], "reference_err": r[k]["truth"]["reference_max_err"]}
+    return {"per_direction_vs_reference": {
+        "source": f"profiles/r02_parity_B{b}.json",
+        "inverse_rel_of_max": r["inverse"]["rel_of_max"],
+        "forward_rel_of_max": r["forward"]["rel_of_max"], "forward_per_slot": r["forward"]["per_slot"],
+        "vs_long_double": {"inverse": truth("inverse"), "dwt_synthesis": truth("inverse_dwt_stage"),
+                           "dwt_analysis": truth("forward_dwt_stage"), "fft_analysis": truth("forward_fft_stage")},
+        "round_trip_gpu": {"max_abs": r["round_trip_gpu"]["max_abs"], "per_slot": r["round_trip_gpu"]["per_slot"],
+                           "rms_abs": r["round_trip_compare"]["gpu_rms_abs"]},
+        "round_trip_reference": {"max_abs": r["round_trip_reference"]["max_abs"],
+                                 "per_slot": r["round_trip_reference"]["per_slot"],
+                                 "rms_abs": r["round_trip_compare"]["reference_rms_abs"]}}}
+
+
 def cpu_whole_measured(b: int):
     """Whole measured runs of the reference arithmetic (profiles/r02_cpu_whole.json)."""
     if not os.path.exists(CPU_WHOLE):
@@ -480,8 +503,8 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
         # passes; the L2 flush between steps is a torch fill, not counted
         "gpu_launches": (2 + 2 * (1 if fused else 2)) * args.steps,
         "clocks": clk,
-        "parity": {"roundtrip_max_abs": rt_abs, "roundtrip_max_rel_per_slot": rt_rel,
-                   "roundtrip_max_rel_of_max": rt_rel_max},
+        "parity": dict({"roundtrip_max_abs": rt_abs, "roundtrip_max_rel_per_slot": rt_rel,
+                        "roundtrip_max_rel_of_max": rt_rel_max}, **committed_parity(b) if F == 1 else {}),
         "peaks": peaks,
     }
     print(json.dumps(line), flush=True)
