@@ -426,6 +426,24 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
                "h2d_bytes_per_step": 16 * F * (C + n ** 3), "d2h_bytes_per_step": 16 * F * (n ** 3 + C),
                "steps": ksteps, "roundtrip_max_abs": e2e_err,
                "api": "ifsoft_sequential(So3Coefficients numpy, pinned) -> fsoft_sequential(So3SampleGrid numpy)"}
+        del h_c, h_g, h_o
+        # the reference's callers pass ordinary (pageable) numpy arrays: the same API with fresh
+        # pageable inputs and outputs, whose copies the driver stages through its own buffers
+        if F == 1:
+            p_c = host_c.copy()
+            def e2e_pageable_step():
+                g = so3.ifsoft_sequential(so3.So3Coefficients(b, p_c), plan)
+                return so3.fsoft_sequential(g, plan)
+            e2e_pageable_step()
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            back = e2e_pageable_step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            p_ms = e0.elapsed_time(e1)
+            e2e["pageable"] = {"value": world * 2000.0 / p_ms, "unit": "transforms/s", "ms_per_step": p_ms,
+                               "steps": 1, "roundtrip_max_abs": float(np.abs(np.asarray(back.data) - host_c).max()),
+                               "api": "ifsoft_sequential / fsoft_sequential on pageable numpy arrays (fresh outputs)"}
 
     if rank != 0:
         return

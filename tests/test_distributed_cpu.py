@@ -67,7 +67,7 @@ def test_sharded_pipeline_matches_single_process(world, b):
     _run(world, b)
 
 
-@pytest.mark.parametrize("world,b,chunks", [(2, 6, 2), (2, 8, 3), (4, 8, 4), (2, 3, 5)])
+@pytest.mark.parametrize("world,b,chunks", [(2, 6, 2), (2, 8, 3), (4, 8, 4), (2, 3, 5), (1, 6, 1), (1, 8, 3)])
 def test_chunked_exchange_pipeline_matches_single_process(world, b, chunks):
     """Exchange split into K chunks (async all_to_all per chunk, DWT per chunk), including
     chunks that are empty on some ranks (B=3, K=5)."""
