@@ -156,8 +156,12 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * "ana_split" (analysis of a cluster over two 4-warp CTAs that combine their halves in a
  * fixed order: 0 = off (one CTA per cluster), 1 = on at 2B = 1024 (default), >= 2 = on at
  * 2B = 512 and 1024; same results to rounding, deterministic; turning it on allocates the
- * partial-sum scratch, 2 x 8 x sum_clusters(B - m) complex128).  All knobs are per plan.  Unknown names fail with
- * SO3_ERR_INVALID. */
+ * partial-sum scratch, 2 x 8 x sum_clusters(B - m) complex128).  Experiment knobs (same results,
+ * measured slower or equal): "fft_persist" (> 0: the
+ * TMA passes as that many persistent double-buffered CTAs), "fft_pad" / "dwt_pad" (extra KB of
+ * shared memory per FFT / MMA DWT CTA), "carveout" (preferred shared-memory carveout of the
+ * big kernels, -1 = driver default; a per-kernel CUDA attribute, re-set by each plan's calls).
+ * All knobs are per plan.  Unknown names fail with SO3_ERR_INVALID. */
 int so3_plan_set_knob(so3_plan_t plan, const char* name, int value);
 
 /* Pair-major spectrum buffer owned by the plan (device pointer, batch x (2B)^3 complex128). */

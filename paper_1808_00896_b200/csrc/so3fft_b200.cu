@@ -49,12 +49,17 @@ int fail(int code, const std::string& msg) {
 bool valid_bandwidth(int b) { return b >= 1 && b <= 4096; }
 constexpr int kMaxBandwidth = 512;   // DWT kernels: at most 2B = 1024 beta indices per cluster
 
-// Shared-memory carveout preference of the big kernels (cudaFuncAttributePreferredSharedMemory-
-// Carveout, a per-kernel, process-wide attribute; -1 = driver default).  Kernels with different
-// carveouts cannot share an SM, so concurrent FFT and DWT launches need the same one.
-int g_carveout = -1;
-// extra KB of dynamic shared memory per MMA DWT CTA (experiments: fewer DWT CTAs per SM)
-int g_dwt_pad = 0;
+// Per-plan launch knobs that act inside the launch helpers (which take kernel arguments, not
+// the plan): each C-ABI stage entry point installs its plan's values for the duration of the
+// call (KnobScope), so they stay per plan.  carveout: cudaFuncAttributePreferredSharedMemory-
+// Carveout of the big kernels (-1 = driver default; kernels with different carveouts cannot
+// share an SM); dwt_pad: extra KB of dynamic shared memory per MMA DWT CTA (experiments with
+// fewer DWT CTAs per SM).
+struct LaunchKnobs {
+  int carveout = -1;
+  int dwt_pad = 0;
+};
+thread_local LaunchKnobs t_knobs;
 
 // The attributes are set once per (kernel, device, value): cudaFuncSetAttribute on a kernel that
 // may be running is not free, and launches on other streams must not wait behind it.
@@ -71,9 +76,9 @@ cudaError_t set_smem(K k, size_t smem) {
   const int cv = it == done.end() ? -1 : it->second.second;
   cudaError_t e = cudaSuccess;
   if (smem > have) e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (!e && g_carveout != cv && g_carveout >= 0)
-    e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, g_carveout);
-  if (!e) done[key] = {std::max(have, smem), g_carveout >= 0 ? g_carveout : cv};
+  const int want = t_knobs.carveout;
+  if (!e && want != cv && want >= 0) e = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, want);
+  if (!e) done[key] = {std::max(have, smem), want >= 0 ? want : cv};
   return e;
 }
 
@@ -210,6 +215,15 @@ struct so3_plan_s {
   int dwt_batch = 1;  // batched plans with 2B <= 64: dense-contraction DWT kernels (dwt_batch.cuh)
   int fft_pad = 0;    // extra KB of shared memory per TMA FFT pass CTA (limits FFT CTAs per SM when co-running)
   int fft_persist = 0;  // > 0: TMA passes as this many persistent double-buffered CTAs (fft_tma.cuh)
+  int carveout = -1;    // see LaunchKnobs
+  int dwt_pad = 0;      // see LaunchKnobs
+};
+
+// installs a plan's LaunchKnobs for one C-ABI call
+struct KnobScope {
+  LaunchKnobs saved;
+  explicit KnobScope(const so3_plan_s* p) : saved(t_knobs) { t_knobs = LaunchKnobs{p->carveout, p->dwt_pad}; }
+  ~KnobScope() { t_knobs = saved; }
 };
 
 // ------------------------------------------------------------------ launches
@@ -597,7 +611,7 @@ inline bool straddles(const so3::DwtArgs& a, int jw) { return a.B % jw != 0; }
 template <int JW, int WPC, int FG = 1>
 int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch, cudaStream_t st) {
   using SM = so3::MmaSmem<JW>;
-  const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double) + (size_t)g_dwt_pad * 1024;
+  const size_t smem = (size_t)WPC * 4 * SM::S * sizeof(double) + (size_t)t_knobs.dwt_pad * 1024;
   auto k = straddles(a, JW) ? so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG, true>
                             : so3::dwt_synthesis_mma_kernel<JW, WPC, (JW <= 64 ? 4 : 2), FG, false>;
   SO3_CUDA(set_smem(k, smem));
@@ -666,7 +680,7 @@ int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cuda
   constexpr int JW = 128;
   const int W = p->n / JW / 2;   // warps per half
   using SM = so3::MmaSmem<JW>;
-  const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double) + (size_t)g_dwt_pad * 1024;
+  const size_t smem = ((size_t)W * 8 * SM::S + 2 * (size_t)W * 512) * sizeof(double) + (size_t)t_knobs.dwt_pad * 1024;
   auto k = so3::dwt_analysis_mma_cta_kernel<JW, 1, 8, 2>;
   SO3_CUDA(set_smem(k, smem));
   k<<<dim3(2 * ncl, 1), W * 32, smem, st>>>(a, sp);
@@ -1157,14 +1171,14 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
   if (k == "fft_tab_tma") { p->fft_tab_tma = value; return SO3_OK; }
   if (k == "fft_bulkin") { p->fft_bulkin = value; return SO3_OK; }
   if (k == "fft_bulkout") { p->fft_bulkout = value; return SO3_OK; }
-  if (k == "carveout") {   // process-wide kernel attribute (see g_carveout)
+  if (k == "carveout") {   // see LaunchKnobs
     if (value < -1 || value > 100) return fail(SO3_ERR_INVALID, "carveout must be -1 or a percentage in [0, 100]");
-    g_carveout = value;
+    p->carveout = value;
     return SO3_OK;
   }
-  if (k == "dwt_pad") {   // process-wide (see g_dwt_pad)
+  if (k == "dwt_pad") {   // see LaunchKnobs
     if (value < 0 || value > 150) return fail(SO3_ERR_INVALID, "dwt_pad must be in [0, 150] KB");
-    g_dwt_pad = value;
+    p->dwt_pad = value;
     return SO3_OK;
   }
   if (k == "fft_persist") {
@@ -1194,6 +1208,7 @@ int so3_plan_set_dwt_variant(so3_plan_t p, int variant) {
 
 int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
+  KnobScope knobs(p);
   if (samples == spectrum || spectrum == p->d_scratch)
     return fail(SO3_ERR_INVALID, "fft_analysis: spectrum must not alias the samples or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1209,6 +1224,7 @@ int so3_fft_analysis(so3_plan_t p, const void* samples, void* spectrum, void* st
 
 int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples); CHECK_PTR(spectrum);
+  KnobScope knobs(p);
   if (samples == spectrum || spectrum == p->d_scratch || samples == p->d_scratch)
     return fail(SO3_ERR_INVALID, "fft_synthesis: buffers must not alias each other or the plan scratch");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1224,11 +1240,13 @@ int so3_fft_synthesis(so3_plan_t p, void* spectrum, void* samples, void* stream)
 
 int so3_dwt_analysis(so3_plan_t p, const void* spectrum, void* coeffs, int64_t c0, int64_t c1, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(spectrum); CHECK_PTR(coeffs);
+  KnobScope knobs(p);
   return launch_dwt<true>(p, spectrum, coeffs, c0, c1, static_cast<cudaStream_t>(stream));
 }
 
 int so3_dwt_synthesis(so3_plan_t p, const void* coeffs, void* spectrum, int64_t c0, int64_t c1, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(spectrum); CHECK_PTR(coeffs);
+  KnobScope knobs(p);
   // the synthesis kernel writes the spectrum; DwtArgs carries it as `spec` and reads `coef`
   return launch_dwt<false>(p, spectrum, const_cast<void*>(coeffs), c0, c1, static_cast<cudaStream_t>(stream));
 }
@@ -1296,6 +1314,7 @@ int so3_ifsoft_host(so3_plan_t p, const void* coeffs_host, void* samples_host, v
 
 int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(slab); CHECK_PTR(send);
+  KnobScope knobs(p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const so3::FftArgs a0 = shard_pass_args(p, 0, slab, p->d_scratch);   // plain strides: TMA-fed when it applies
   int rc = launch_fft_tma(p, a0, +1, st);
@@ -1310,12 +1329,14 @@ int so3_shard_fft_analysis(so3_plan_t p, const void* slab, void* send, void* str
 // chunk q of layout B starts at row world * chunk_off[q]
 int so3_shard_dwt_analysis_chunk(so3_plan_t p, int q, const void* recv_chunk, void* coeffs, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_CHUNK(p, q); CHECK_PTR(recv_chunk); CHECK_PTR(coeffs);
+  KnobScope knobs(p);
   return launch_dwt<true>(p, recv_chunk, coeffs, p->chunk_cl[q], p->chunk_cl[q + 1], static_cast<cudaStream_t>(stream),
                           p->chunk_pairs[q]);
 }
 
 int so3_shard_dwt_synthesis_chunk(so3_plan_t p, int q, const void* coeffs, void* send_chunk, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_CHUNK(p, q); CHECK_PTR(coeffs); CHECK_PTR(send_chunk);
+  KnobScope knobs(p);
   return launch_dwt<false>(p, send_chunk, const_cast<void*>(coeffs), p->chunk_cl[q], p->chunk_cl[q + 1],
                            static_cast<cudaStream_t>(stream), p->chunk_pairs[q]);
 }
@@ -1340,6 +1361,7 @@ int so3_shard_dwt_synthesis(so3_plan_t p, const void* coeffs, void* send, void* 
 
 int so3_shard_fft_synthesis(so3_plan_t p, const void* recv, void* slab, void* stream) {
   CHECK_PLAN(p); CHECK_SHARD(p); CHECK_PTR(recv); CHECK_PTR(slab);
+  KnobScope knobs(p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = launch_fft(p, shard_pass_args(p, 2, recv, p->d_scratch), -1, 1, st);
   if (rc) return rc;
