@@ -754,7 +754,7 @@ def main() -> None:
                     help="rendezvous only (gloo): every rank reports in, rank 0 prints the ranks it saw")
     args = ap.parse_args()
     if args.cpu_stride <= 0:
-        args.cpu_stride = {512: 64, 256: 8}.get(args.bandwidth, 1)
+        args.cpu_stride = {512: 32, 256: 4}.get(args.bandwidth, 1)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the timing rules require >= 3 warm-up steps", file=sys.stderr)
 
