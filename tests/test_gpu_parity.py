@@ -721,3 +721,38 @@ def test_streamed_containers_device_side(tmp_path, golden):
     bad[12345] = complex(float("nan"), 0.0)
     with pytest.raises(ValueError, match="non-finite"):
         so3.write_samples(str(tmp_path / "bad.sofg"), so3.So3SampleGrid(b, bad))
+
+
+# ---------------------------------------------------------------- bandwidths off the power-of-two grid
+
+@pytest.mark.parametrize("b", [72, 100])
+def test_non_power_of_two_bandwidths_match_oracle(b):
+    """2B not a power of two: direct-DFT slice passes, and warps whose beta indices straddle
+    pi/2 (B not a multiple of the warp's beta span JW = 64), which take the per-index branch of
+    the accurate recurrence (common.cuh rec_t, dwt_mma.cuh STR).  Both directions against the
+    reference arithmetic on the same inputs (soft.py:124-173)."""
+    rng = np.random.default_rng(b)
+    c = rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))
+    plan = plan_for(b)
+    g = so3.ifsoft_sequential(so3.So3Coefficients(b, torch.from_numpy(c).cuda()), plan).data.cpu().numpy()
+    g_ref = O.ifsoft(c, b, O.default_workers())
+    assert rel_of_max(g, g_ref) < 1e-12
+    f = so3.fsoft_sequential(so3.So3SampleGrid(b, torch.from_numpy(g_ref).cuda()), plan).data.cpu().numpy()
+    f_ref = O.fsoft(g_ref, b, O.default_workers())
+    assert rel_of_max(f, f_ref) < 1e-12
+    assert per_slot(f, f_ref) < 1e-10
+
+
+def test_bandwidth_limits():
+    """1 <= B <= 512 on one device; B = 513 is rejected at plan creation with ValueError
+    (the DWT kernels hold at most 2B = 1024 beta indices per cluster), not at transform time."""
+    with pytest.raises(ValueError, match="512"):
+        so3.make_plan(513)
+    with pytest.raises(ValueError):
+        so3.make_plan(0)
+    b = 300                        # 2B = 600: five 128-beta warps, one straddling pi/2
+    rng = np.random.default_rng(300)
+    c = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    plan = plan_for(b)
+    back = so3.fsoft_sequential(so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan), plan).data
+    assert float((back - c).abs().max()) < 1e-11
