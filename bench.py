@@ -547,13 +547,12 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     stream = torch.cuda.current_stream(dev)
     host_c = seeded_coefficients(b, b)
     coeffs = torch.from_numpy(host_c).to(dev)
-    # staged step (one chunk): buffers reused across steps (the exchange is the only collective);
-    # the pipelined step allocates through ShardedSO3 (torch's caching allocator reuses them)
+    # staged step (one chunk): one exchange buffer (layout A, then layout B with the own block)
+    # reused across steps; the pipelined step allocates through ShardedSO3 (torch's caching
+    # allocator reuses them)
     if chunks == 1:
-        send_b = backend.empty(m.layout_b_rows(rank) * J)
-        recv_a = backend.empty(m.layout_a_rows() * J)
-        send_a = backend.empty(m.layout_a_rows() * J)
-        recv_b = backend.empty(m.layout_b_rows(rank) * J)
+        ex = backend.empty(m.exchange_rows(rank) * J)
+        lay_b = ex[m.b_chunk(rank, 0)[0]:]
         slab = backend.empty(n * J * n)
     out = backend.zeros(C)
 
@@ -562,20 +561,19 @@ def run_sharded_arm(args, rank: int, world: int, dist) -> None:
     def step_staged(evs=None):
         rec = (lambda i: evs[i].record(stream)) if evs is not None else (lambda i: None)
         rec(0)
-        # one rank: layouts A and B coincide, so the exchange is elided (ShardedSO3 does the same)
-        backend.dwt_synthesis(coeffs, send_b)
+        backend.dwt_synthesis(coeffs, lay_b)
         rec(1)
-        if world > 1:
-            sh._all_to_all(recv_a, send_b, m.inverse_recv_splits(rank), m.inverse_send_splits(rank))
+        for w in sh._exchange(ex, 0, forward=False):   # other ranks' blocks only (none for one rank)
+            w.wait()
         rec(2)
-        backend.fft_synthesis(recv_a if world > 1 else send_b, slab)
+        backend.fft_synthesis(ex, slab)
         rec(3)
-        backend.fft_analysis(slab, send_a)
+        backend.fft_analysis(slab, ex)
         rec(4)
-        if world > 1:
-            sh._all_to_all(recv_b, send_a, m.forward_recv_splits(rank), m.forward_send_splits(rank))
+        for w in sh._exchange(ex, 0, forward=True):
+            w.wait()
         rec(5)
-        backend.dwt_analysis(recv_b if world > 1 else send_a, out)
+        backend.dwt_analysis(lay_b, out)
         rec(6)
         result["coeffs"] = out
 

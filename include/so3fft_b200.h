@@ -181,6 +181,11 @@ void* so3_plan_scratch(so3_plan_t plan);
  *   layout B : rows [chunk q][rank h][pairs_{rank,q}][J] (forward recv / inverse send,
  *              G * pairs_rank * J); chunk q starts at row G * sum_{q' < q} pairs_{rank,q'}
  *   coeffs   : full l-major array; a rank writes (forward) / reads (inverse) only its slots.
+ *   exchange : ONE buffer holding layout A (rows [0, (2B-1)^2)) followed by layout B.  The
+ *              rank's own block (g = h = rank of every chunk) exists in layout B only: the
+ *              forward FFT stores the own pairs straight into layout B and the inverse FFT
+ *              reads them from there, so the all-to-all moves the other ranks' blocks only
+ *              (no self copy; the layout-A rows of the own block are left unused).
  * Results are identical, bit for bit, for every G and K (the same per-row FFTs and
  * per-cluster reductions run whatever the split).  K = 1 is the unchunked exchange. */
 int so3_shard_plan_create(int bandwidth, int world, int rank, so3_plan_t* out);      /* K = 1 */
@@ -194,8 +199,9 @@ int so3_shard_pair_counts(int bandwidth, int world, int64_t* pairs_per_rank);
 int so3_shard_cluster_owner(int bandwidth, int world, int32_t* owner);
 int so3_shard_pair_list(int bandwidth, int world, int rank, int32_t* pairs);
 int so3_shard_chunk_pairs(int bandwidth, int world, int chunks, int64_t* pairs);
-/* forward: slab -> layout A (K1a + K1b with the pack fused into the store) */
-int so3_shard_fft_analysis(so3_plan_t plan, const void* slab_dev, void* send_dev, void* stream);
+/* forward: slab -> exchange buffer (K1a + K1b with the pack fused into the store): other
+ * ranks' pairs into layout A, the own pairs into layout B */
+int so3_shard_fft_analysis(so3_plan_t plan, const void* slab_dev, void* exchange_dev, void* stream);
 /* forward: layout B -> this rank's coefficient slots */
 int so3_shard_dwt_analysis(so3_plan_t plan, const void* recv_dev, void* coeffs_dev, void* stream);
 /* inverse: this rank's coefficient slots -> layout B */
@@ -205,8 +211,9 @@ int so3_shard_dwt_analysis_chunk(so3_plan_t plan, int chunk, const void* recv_ch
                                  void* stream);
 int so3_shard_dwt_synthesis_chunk(so3_plan_t plan, int chunk, const void* coeffs_dev, void* send_chunk_dev,
                                   void* stream);
-/* inverse: layout A -> slab (K4a with the unpack fused into the load, K4b) */
-int so3_shard_fft_synthesis(so3_plan_t plan, const void* recv_dev, void* slab_dev, void* stream);
+/* inverse: exchange buffer -> slab (K4a with the unpack fused into the load, K4b): other
+ * ranks' pairs from layout A, the own pairs from layout B */
+int so3_shard_fft_synthesis(so3_plan_t plan, const void* exchange_dev, void* slab_dev, void* stream);
 
 /* Direct O(B^6) transforms (fsoft_direct / ifsoft_direct, soft.py:212-256): the defining
  * sums over closed-form Wigner functions (wigner.py:78-114), sharing nothing with the fast

@@ -1062,6 +1062,22 @@ int so3_shard_plan_create_chunked(int b, int world, int rank, int chunks, so3_pl
   p->chunk_off.assign(chunks + 1, 0);
   for (int q = 0; q < chunks; ++q) p->chunk_off[q + 1] = p->chunk_off[q] + p->chunk_pairs[q];
   p->pairs_rank = p->pairs_of[rank];
+  // Self-block elision: the FFT passes address ONE exchange buffer holding layout A (rows
+  // [0, rows_A)) followed by layout B.  This rank's own pairs live in layout B only (block
+  // h = rank of each chunk), so the forward FFT writes them where the DWT reads them and the
+  // inverse FFT reads them where the DWT wrote them: the all-to-all carries the other ranks'
+  // blocks only.
+  const int64_t rows_a = base_a.back();
+  for (size_t i = 0; i < all.size(); ++i) {
+    if (owner[i] != rank) continue;
+    const int q = chunk_of[i];
+    for (const auto& pr : cluster_pairs(all[i].m, all[i].mp)) {
+      const int bm = ((pr.first % n) + n) % n, bmp = ((pr.second % n) + n) % n;
+      const size_t idx = (size_t)bmp * n + bm;
+      row_global[idx] = (int)(rows_a + (int64_t)world * p->chunk_off[q] + (int64_t)rank * p->chunk_pairs[q] +
+                              row_local[idx]);
+    }
+  }
   int rc = build_plan(p, mine);
   if (rc) { so3_plan_destroy(p); return rc; }
   cudaError_t e = cudaMalloc((void**)&p->d_row_global, row_global.size() * sizeof(int));

@@ -14,10 +14,14 @@ B200 box, gloo in the CPU tests), split into K chunks of clusters so the exchang
 the DWT: forward, the all-to-alls of all chunks are queued behind the FFT and the DWT of
 chunk q starts as soon as chunk q has arrived; inverse, chunk q is sent while chunk q+1 is
 synthesised.  Pack and unpack are fused into the FFT kernels through a pair -> row table,
-so the exchange moves the FFT output / DWT output buffers directly:
+so the exchange moves the FFT output / DWT output buffers directly.  One exchange buffer per
+direction holds both layouts:
 
   layout A  rows [chunk q][rank g][pairs_{g,q}][J]      forward send, inverse recv
   layout B  rows [chunk q][rank h][pairs_{rank,q}][J]   forward recv, inverse send
+
+and the rank's own block exists in layout B only (the FFT writes / reads the own pairs there),
+so the all-to-all carries the other ranks' blocks and no self copy.
 
 Results are bit-identical for every G and K (the same per-row FFTs and per-cluster
 reductions run whatever the split).  Coefficients stay sharded: a rank writes / reads only the slots of its
@@ -90,6 +94,26 @@ class ShardMap:
     def chunk_b(self, rank: int, q: int) -> tuple[int, int]:
         start = self.world * sum(self.chunk_pairs[p][rank] for p in range(q)) * self.J
         return start, start + self.world * self.chunk_pairs[q][rank] * self.J
+
+    # the exchange buffer of `rank`: layout A rows, then layout B rows (own block in B only)
+    def exchange_rows(self, rank: int) -> int:
+        return self.layout_a_rows() + self.layout_b_rows(rank)
+
+    def a_block(self, q: int, g: int) -> tuple[int, int]:
+        """element range of layout A block (chunk q, rank g) in the exchange buffer"""
+        start = sum(sum(self.chunk_pairs[p]) for p in range(q)) + sum(self.chunk_pairs[q][:g])
+        return start * self.J, (start + self.chunk_pairs[q][g]) * self.J
+
+    def b_block(self, rank: int, q: int, h: int) -> tuple[int, int]:
+        """element range of layout B block (chunk q, source slab h) in `rank`'s exchange buffer"""
+        start = self.layout_a_rows() + self.world * sum(self.chunk_pairs[p][rank] for p in range(q)) \
+            + h * self.chunk_pairs[q][rank]
+        return start * self.J, (start + self.chunk_pairs[q][rank]) * self.J
+
+    def b_chunk(self, rank: int, q: int) -> tuple[int, int]:
+        """element range of layout B chunk q (all source slabs) in `rank`'s exchange buffer"""
+        a0 = self.b_block(rank, q, 0)[0]
+        return a0, a0 + self.world * self.chunk_pairs[q][rank] * self.J
 
     # all_to_all_single split sizes of chunk q, in complex128 elements
     def forward_send_splits(self, rank: int, q: int = 0) -> list[int]:
@@ -202,15 +226,27 @@ class ShardedSO3:
         self.coeff_count = coeff_count(self.bandwidth)
         self.slab_count = self.map.n * self.map.J * self.map.n
 
-    def _all_to_all(self, recv, send, recv_splits, send_splits, async_op=False):
+    def _exchange(self, ex, q: int, forward: bool):
+        """One chunk of the all-to-all on the exchange buffer, the other ranks' blocks only
+        (the own block already sits in layout B): forward sends layout A blocks (q, g) and
+        receives layout B blocks (q, h); the inverse the reverse.  Grouped point-to-point
+        operations (one NCCL group per chunk; gloo in the CPU tests), since a collective over
+        all ranks would carry the self block.  Returns the pending works."""
         import torch.distributed as dist
-        if self.world == 1 and not (dist.is_available() and dist.is_initialized()):
-            recv.copy_(send)
-            return None
-        return dist.all_to_all_single(_as_real(recv), _as_real(send),
-                                      output_split_sizes=[2 * s for s in recv_splits],
-                                      input_split_sizes=[2 * s for s in send_splits], group=self.group,
-                                      async_op=async_op)
+        if self.world == 1:
+            return []
+        m, r = self.map, self.rank
+        ops = []
+        for peer in range(self.world):
+            if peer == r:
+                continue
+            a = _as_real(ex[slice(*m.a_block(q, peer))])       # pairs of `peer`, this rank's slab
+            b = _as_real(ex[slice(*m.b_block(r, q, peer))])    # this rank's pairs, slab of `peer`
+            if forward:
+                ops += [dist.P2POp(dist.isend, a, peer, self.group), dist.P2POp(dist.irecv, b, peer, self.group)]
+            else:
+                ops += [dist.P2POp(dist.isend, b, peer, self.group), dist.P2POp(dist.irecv, a, peer, self.group)]
+        return dist.batch_isend_irecv(ops)
 
     def fsoft(self, slab, out=None):
         """This rank's beta slab [i][jj][k] -> coefficients: this rank's slots are written, the
@@ -219,55 +255,30 @@ class ShardedSO3:
         All chunk exchanges are queued behind the FFT; the DWT of chunk q waits for chunk q
         only (on the device stream for NCCL), so it overlaps the exchange of chunks > q."""
         m, r = self.map, self.rank
-        send = self.backend.empty(m.layout_a_rows() * m.J)
-        self.backend.fft_analysis(slab, send)
-        if self.world == 1:
-            # one rank: layouts A and B coincide (every block is the rank's own), no exchange
-            coeffs = self.backend.zeros(self.coeff_count) if out is None else out
-            for q in range(self.chunks):
-                b0, b1 = m.chunk_b(r, q)
-                self.backend.dwt_analysis_chunk(q, send[b0:b1], coeffs)
-            return coeffs
-        recv = self.backend.empty(m.layout_b_rows(r) * m.J)
-        works = []
-        for q in range(self.chunks):
-            a0, a1 = m.chunk_a(q)
-            b0, b1 = m.chunk_b(r, q)
-            works.append(self._all_to_all(recv[b0:b1], send[a0:a1], m.forward_recv_splits(r, q),
-                                          m.forward_send_splits(r, q), async_op=True))
+        ex = self.backend.empty(m.exchange_rows(r) * m.J)
+        self.backend.fft_analysis(slab, ex)
+        works = [self._exchange(ex, q, forward=True) for q in range(self.chunks)]
         coeffs = self.backend.zeros(self.coeff_count) if out is None else out
         for q in range(self.chunks):
-            if works[q] is not None:
-                works[q].wait()
-            b0, b1 = m.chunk_b(r, q)
-            self.backend.dwt_analysis_chunk(q, recv[b0:b1], coeffs)
+            for w in works[q]:
+                w.wait()
+            self.backend.dwt_analysis_chunk(q, ex[slice(*m.b_chunk(r, q))], coeffs)
         return coeffs
 
     def ifsoft(self, coeffs):
         """Coefficients (this rank's slots are read) -> this rank's beta slab [i][jj][k].
         Chunk q is exchanged while chunk q+1 is synthesised."""
         m, r = self.map, self.rank
-        send = self.backend.empty(m.layout_b_rows(r) * m.J)
-        if self.world == 1:   # layouts A and B coincide: the DWT output is the FFT input
-            for q in range(self.chunks):
-                b0, b1 = m.chunk_b(r, q)
-                self.backend.dwt_synthesis_chunk(q, coeffs, send[b0:b1])
-            slab = self.backend.empty(self.slab_count)
-            self.backend.fft_synthesis(send, slab)
-            return slab
-        recv = self.backend.empty(m.layout_a_rows() * m.J)
+        ex = self.backend.empty(m.exchange_rows(r) * m.J)
         works = []
         for q in range(self.chunks):
-            b0, b1 = m.chunk_b(r, q)
-            a0, a1 = m.chunk_a(q)
-            self.backend.dwt_synthesis_chunk(q, coeffs, send[b0:b1])
-            works.append(self._all_to_all(recv[a0:a1], send[b0:b1], m.inverse_recv_splits(r, q),
-                                          m.inverse_send_splits(r, q), async_op=True))
-        for w in works:
-            if w is not None:
+            self.backend.dwt_synthesis_chunk(q, coeffs, ex[slice(*m.b_chunk(r, q))])
+            works.append(self._exchange(ex, q, forward=False))
+        for ws in works:
+            for w in ws:
                 w.wait()
         slab = self.backend.empty(self.slab_count)
-        self.backend.fft_synthesis(recv, slab)
+        self.backend.fft_synthesis(ex, slab)
         return slab
 
     def gather_coefficients(self, coeffs):

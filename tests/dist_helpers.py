@@ -1,7 +1,8 @@
 """Numpy stand-in for the four sharded stage kernels (test infrastructure: lets the gloo
 tests run the real shard map + exchange orchestration of paper_1808_00896_b200.distributed
 on CPU).  Layouts follow include/so3fft_b200.h: slab [i][jj][k], layout A rows
-[q][g][pairs_{g,q}][J], layout B rows [q][h][pairs_{rank,q}][J] (chunk-major)."""
+[q][g][pairs_{g,q}][J], layout B rows [q][h][pairs_{rank,q}][J] (chunk-major), both in one
+exchange buffer (A first) with the rank's own pairs in layout B only."""
 import math
 
 import numpy as np
@@ -33,6 +34,9 @@ class NumpyShardBackend:
                     if g == rank:
                         self.local[pair] = (q, i)
                 off[g] += cp[q][g]
+        # exchange buffer = layout A then layout B: the own pairs live in layout B only
+        for pair, (q, i) in self.local.items():
+            self.glob[pair] = self.map.b_block(rank, q, rank)[0] // self.J + i
         bases, _ = cluster_schedule(b)
         owner = self.map.cluster_owner()
         self.clusters = [[] for _ in range(chunks)]
@@ -50,7 +54,7 @@ class NumpyShardBackend:
     def zeros(self, count):
         return torch.zeros(count, dtype=torch.complex128)
 
-    def fft_analysis(self, slab, send):
+    def fft_analysis(self, slab, send):   # send: the exchange buffer
         n, J = self.n, self.J
         s = slab.numpy().reshape(n, J, n)
         out = send.numpy()

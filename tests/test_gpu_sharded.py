@@ -16,47 +16,49 @@ def emulate(b, world, grid, coeffs, chunks=1):
     n = 2 * b
     m = ShardMap(b, world, chunks)
     J = m.J
-    cp = m.chunk_pairs
     be = [NativeShardBackend(b, world, r, chunks=chunks) for r in range(world)]
     cube = grid.reshape(n, n, n)
-    # forward: FFT per slab, then chunk by chunk exchange (device copies) + per-chunk DWT
-    sends = []
+    # forward: FFT per slab into each rank's exchange buffer (own pairs already in layout B),
+    # the all-to-all of the other blocks done by device copies, then each rank's chunked DWT
+    ex = []
     for r in range(world):
         slab = cube[:, r * J:(r + 1) * J, :].contiguous().reshape(-1)
-        s = be[r].empty(m.layout_a_rows() * J)
-        be[r].fft_analysis(slab, s)
-        sends.append(s)
+        e = be[r].empty(m.exchange_rows(r) * J)
+        be[r].fft_analysis(slab, e)
+        ex.append(e)
     out = torch.zeros_like(coeffs)
     for g in range(world):
         c = be[g].zeros(out.numel())
         for q in range(chunks):
-            a0 = m.chunk_a(q)[0] + sum(cp[q][:g]) * J
-            recv = torch.cat([sends[h][a0:a0 + cp[q][g] * J] for h in range(world)])
-            be[g].dwt_analysis_chunk(q, recv, c)
+            for h in range(world):
+                if h != g:
+                    ex[g][slice(*m.b_block(g, q, h))] = ex[h][slice(*m.a_block(q, g))]
+            be[g].dwt_analysis_chunk(q, ex[g][slice(*m.b_chunk(g, q))], c)
         out += c
-    # inverse: per-chunk synthesis into layout B, exchange, FFT per slab
-    sends = []
+    del ex, c
+    torch.cuda.empty_cache()
+    # inverse: per-chunk synthesis into layout B, exchange of the other blocks, FFT per slab
+    ex = [be[g].empty(m.exchange_rows(g) * J) for g in range(world)]
     for g in range(world):
-        s = be[g].empty(m.layout_b_rows(g) * J)
         for q in range(chunks):
-            b0, b1 = m.chunk_b(g, q)
-            be[g].dwt_synthesis_chunk(q, coeffs, s[b0:b1])
-        sends.append(s)
+            be[g].dwt_synthesis_chunk(q, coeffs, ex[g][slice(*m.b_chunk(g, q))])
+    for g in range(world):
+        for q in range(chunks):
+            for h in range(world):
+                if h != g:
+                    ex[h][slice(*m.a_block(q, g))] = ex[g][slice(*m.b_block(g, q, h))]
     slabs = []
     for h in range(world):
-        parts = []
-        for q in range(chunks):
-            for g in range(world):
-                b0 = m.chunk_b(g, q)[0] + h * cp[q][g] * J
-                parts.append(sends[g][b0:b0 + cp[q][g] * J])
-        recv = torch.cat(parts)
         slab = be[h].empty(n * J * n)
-        be[h].fft_synthesis(recv, slab)
+        be[h].fft_synthesis(ex[h], slab)
         slabs.append(slab.reshape(n, J, n))
+    del ex
     back = torch.cat(slabs, dim=1).reshape(-1)
+    del slabs
     torch.cuda.synchronize()
     for x in be:
         x.release()
+    torch.cuda.empty_cache()
     return out, back
 
 
@@ -72,9 +74,12 @@ def test_sharded_equals_single_gpu_bitwise(b, world, chunks):
     plan = so3.make_plan(b)
     ref_f = so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan).data
     ref_i = so3.ifsoft_sequential(so3.So3Coefficients(b, coeffs), plan).data
+    plan.release()
     got_f, got_i = emulate(b, world, grid, coeffs, chunks)
     assert torch.equal(got_f, ref_f)
     assert torch.equal(got_i, ref_i)
+    del grid, got_f, got_i, ref_f, ref_i
+    torch.cuda.empty_cache()
 
 
 def test_full_dwt_entry_points_walk_all_chunks():
@@ -104,7 +109,7 @@ def test_full_dwt_entry_points_walk_all_chunks():
 @pytest.mark.parametrize("chunks", [1, 3])
 def test_sharded_bench_under_torchrun_nccl(chunks):
     """The multi-GPU bench arm end to end under torchrun with one rank: NCCL process group,
-    all_to_all_single per chunk (self exchange), e2e, max-over-ranks timing; the gathered
+    the per-chunk exchange (no peers with one rank), e2e, max-over-ranks timing; the gathered
     round trip must recover the seeded coefficients."""
     import json
     import os

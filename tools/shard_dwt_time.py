@@ -23,9 +23,9 @@ for name, fn in (("dwt_synthesis", lambda: be.dwt_synthesis(coef, send)), ("dwt_
     print(f"B={b} G={world} rank0 {name}: {e0.elapsed_time(e1) / 3:.3f} ms")
 n, J = 2 * b, m.J
 slab = torch.from_numpy(rng.standard_normal(n * J * n) + 1j * rng.standard_normal(n * J * n)).cuda()
-send_a = be.empty(m.layout_a_rows() * J)
+ex = be.empty(m.exchange_rows(0) * J)   # layout A, then layout B with the own block
 out_slab = be.empty(n * J * n)
-for name, fn in (("fft_analysis", lambda: be.fft_analysis(slab, send_a)), ("fft_synthesis", lambda: be.fft_synthesis(send_a, out_slab))):
+for name, fn in (("fft_analysis", lambda: be.fft_analysis(slab, ex)), ("fft_synthesis", lambda: be.fft_synthesis(ex, out_slab))):
     fn(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record(); [fn() for _ in range(3)]; e1.record(); torch.cuda.synchronize()
