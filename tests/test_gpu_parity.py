@@ -756,3 +756,63 @@ def test_bandwidth_limits():
     plan = plan_for(b)
     back = so3.fsoft_sequential(so3.ifsoft_sequential(so3.So3Coefficients(b, c), plan), plan).data
     assert float((back - c).abs().max()) < 1e-11
+
+
+# ---------------------------------------------------------------- launch-path properties
+
+def test_transforms_capture_into_a_cuda_graph():
+    """Device entry points allocate nothing on the launch path (the split-analysis scratch and
+    counters are made at plan creation), so a whole iFSOFT -> FSOFT step captures into one CUDA
+    graph; replays reproduce the eager results bit for bit (B = 512 would take 17 GB per
+    buffer, so 2B = 512 with the split analysis switched on stands in for it)."""
+    b = 256
+    plan = plan_for(b)
+    plan.set_knob("ana_split", 2)    # split analysis at 2B = 512 (scratch allocated here, not at launch)
+    rng = np.random.default_rng(11)
+    c = torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+    grid = torch.empty((2 * b) ** 3, dtype=torch.complex128, device="cuda")
+    spec = torch.empty_like(grid)
+    out = torch.empty_like(c)
+
+    def step():
+        so3.dwt_synthesis(plan, c, spec)
+        so3.fft_synthesis(plan, spec, grid)
+        so3.fft_analysis(plan, grid, spec)
+        so3.dwt_analysis(plan, spec, out)
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()                       # warm-up on the capture stream (kernel attributes, maps)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = out.clone()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    out.zero_()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    assert float((eager - c).abs().max()) < 1e-11
+
+
+def test_independent_plans_on_concurrent_streams():
+    """Calls on ONE plan are stream-ordered (its scratch is shared, include/so3fft_b200.h);
+    separate plans on separate streams run concurrently and give the sequential results."""
+    b = 64
+    rng = np.random.default_rng(12)
+    cs = [torch.from_numpy(rng.standard_normal(O.n_coeffs(b)) + 1j * rng.standard_normal(O.n_coeffs(b))).cuda()
+          for _ in range(2)]
+    plans = [plan_for(b), plan_for(b)]
+    ref = [so3.ifsoft_sequential(so3.So3Coefficients(b, c), p).data.clone() for c, p in zip(cs, plans)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    outs = [None, None]
+    for _ in range(5):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                outs[k] = so3.ifsoft_sequential(so3.So3Coefficients(b, cs[k]), plans[k]).data
+    torch.cuda.synchronize()
+    assert all(torch.equal(o, r) for o, r in zip(outs, ref))
