@@ -110,7 +110,11 @@ int so3_ifsoft(so3_plan_t plan, const void* coeffs_dev, void* samples_dev, void*
 
 /* Same with HOST buffers: copies in, transforms, copies out, and synchronises
  * `stream` before returning (the reference API's numpy-in / numpy-out contract).
- * Device staging buffers are allocated on first use and kept by the plan. */
+ * Device staging buffers are allocated on first use and kept by the plan.
+ * Pinned (page-locked / registered) host buffers are copied directly; pageable buffers of
+ * 64 MB or more go through the plan's pinned bounce buffers (2 x 16 MB per worker, one
+ * worker thread per host core up to 16, allocated on the first pageable call), so the
+ * host-side copies and first-touch page faults run in parallel with the DMA (hostio.cuh). */
 int so3_fsoft_host(so3_plan_t plan, const void* samples_host, void* coeffs_host, void* stream);
 int so3_ifsoft_host(so3_plan_t plan, const void* coeffs_host, void* samples_host, void* stream);
 

@@ -23,6 +23,7 @@
 #include "../../include/so3fft_b200.h"
 #include "common.cuh"
 #include "sofio.cuh"
+#include "hostio.cuh"
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
 #include "dwt_batch.cuh"
@@ -188,6 +189,7 @@ struct so3_plan_s {
   // staging for the host-buffer entry points
   double2* d_grid_stage = nullptr;
   double2* d_coef_stage = nullptr;
+  so3host::Staging host_stage;         // pinned bounce buffers for pageable host buffers (hostio.cuh)
   int64_t bytes = 0;
   // sharding (world > 1 or a sharded plan): beta slab [jbase, jbase + J) and a cluster group
   int sharded = 0, world = 1, rank = 0, J = 0, jbase = 0;
@@ -1157,6 +1159,7 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_row_local);
   cudaFree(p->d_grid_stage);
   cudaFree(p->d_coef_stage);
+  p->host_stage.release();
   delete p;
 }
 
@@ -1295,17 +1298,38 @@ static int ensure_stage(so3_plan_t p) {
   return SO3_OK;
 }
 
+// Host <-> device copy of a host-buffer entry point: pinned buffers (and small pageable ones)
+// go straight to the DMA engines on the caller's stream; large pageable buffers through the
+// plan's multi-threaded pinned staging (hostio.cuh), ordered after the stream's earlier work.
+static int host_copy(so3_plan_t p, void* dev, void* host, size_t bytes, bool to_device, cudaStream_t st) {
+  constexpr size_t kDirect = size_t(64) << 20;
+  if (bytes < kDirect || so3host::is_pinned(host)) {
+    SO3_CUDA(cudaMemcpyAsync(to_device ? dev : host, to_device ? (const void*)host : (const void*)dev, bytes,
+                             to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, st));
+    return SO3_OK;
+  }
+  if (!p->host_stage.ready()) {
+    const cudaError_t e = p->host_stage.init(p->device, so3host::default_workers(), so3host::kChunk);
+    if (e != cudaSuccess) return fail(SO3_ERR_NOMEM, std::string("pinned staging: ") + cudaGetErrorString(e));
+  }
+  SO3_CUDA(cudaStreamSynchronize(st));
+  SO3_CUDA(to_device ? p->host_stage.run<+1>(p->device, dev, host, bytes)
+                     : p->host_stage.run<-1>(p->device, dev, host, bytes));
+  return SO3_OK;
+}
+
 int so3_fsoft_host(so3_plan_t p, const void* samples_host, void* coeffs_host, void* stream) {
   CHECK_PLAN(p); CHECK_PTR(samples_host); CHECK_PTR(coeffs_host);
   int rc = ensure_stage(p);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SO3_CUDA(cudaMemcpyAsync(p->d_grid_stage, samples_host, (size_t)p->ngrid * p->batch * sizeof(double2),
-                           cudaMemcpyHostToDevice, st));
+  rc = host_copy(p, p->d_grid_stage, const_cast<void*>(samples_host), (size_t)p->ngrid * p->batch * sizeof(double2),
+                 true, st);
+  if (rc) return rc;
   rc = so3_fsoft(p, p->d_grid_stage, p->d_coef_stage, stream);
   if (rc) return rc;
-  SO3_CUDA(cudaMemcpyAsync(coeffs_host, p->d_coef_stage, (size_t)p->ncoef * p->batch * sizeof(double2),
-                           cudaMemcpyDeviceToHost, st));
+  rc = host_copy(p, p->d_coef_stage, coeffs_host, (size_t)p->ncoef * p->batch * sizeof(double2), false, st);
+  if (rc) return rc;
   SO3_CUDA(cudaStreamSynchronize(st));
   return SO3_OK;
 }
@@ -1315,12 +1339,13 @@ int so3_ifsoft_host(so3_plan_t p, const void* coeffs_host, void* samples_host, v
   int rc = ensure_stage(p);
   if (rc) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  SO3_CUDA(cudaMemcpyAsync(p->d_coef_stage, coeffs_host, (size_t)p->ncoef * p->batch * sizeof(double2),
-                           cudaMemcpyHostToDevice, st));
+  rc = host_copy(p, p->d_coef_stage, const_cast<void*>(coeffs_host), (size_t)p->ncoef * p->batch * sizeof(double2),
+                 true, st);
+  if (rc) return rc;
   rc = so3_ifsoft(p, p->d_coef_stage, p->d_grid_stage, stream);
   if (rc) return rc;
-  SO3_CUDA(cudaMemcpyAsync(samples_host, p->d_grid_stage, (size_t)p->ngrid * p->batch * sizeof(double2),
-                           cudaMemcpyDeviceToHost, st));
+  rc = host_copy(p, p->d_grid_stage, samples_host, (size_t)p->ngrid * p->batch * sizeof(double2), false, st);
+  if (rc) return rc;
   SO3_CUDA(cudaStreamSynchronize(st));
   return SO3_OK;
 }
