@@ -27,6 +27,7 @@
 #include "dwt.cuh"
 #include "dwt_mma.cuh"
 #include "dwt_batch.cuh"
+#include "dwt_seg.cuh"
 #include "fft.cuh"
 #include "fft_tma.cuh"
 #include "direct.cuh"
@@ -207,6 +208,11 @@ struct so3_plan_s {
   long long rc_entries = 0;       // recurrence-table entries = sum over the plan's clusters of (B - m)
   double2* d_pbuf = nullptr;      // split analysis: per-half partial sums, 2 x rc_entries x 8
   unsigned* d_pcnt = nullptr;     // split analysis: per-cluster arrival counters
+  // segment-parallel DWT (dwt_seg.cuh): checkpoint table [cluster][8][2B] of recurrence states
+  int dwt_seg = 1;                // knob, bits: 1 = segment-parallel synthesis, 2 = analysis (where B % 64 == 0)
+  int seg_ana_w = 8;              // knob: most warps per analysis CTA (8: one CTA per SM; 4: two)
+  double2* d_ck = nullptr;
+  int pbuf_splits = 0;            // partial sets d_pbuf holds
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
   int fft_tma = 1;    // TMA-fed FFT kernels (fft_tma.cuh): passes at 2B in {256, 512, 1024}, one-pass slices
@@ -690,6 +696,58 @@ int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cuda
   return SO3_OK;
 }
 
+// Segment-parallel kernels (dwt_seg.cuh): B a multiple of 64, the plan's checkpoint table built.
+bool seg_eligible(const so3_plan_s* p) { return p->B >= 64 && p->B % 64 == 0 && p->B <= 512; }
+bool seg_applies(const so3_plan_s* p) {
+  return p->dwt_seg && p->d_ck && p->dwt_variant != SO3_DWT_SIMT && seg_eligible(p);
+}
+// CTAs per cluster of the segment-parallel analysis: the fewest of {1, 2, 4} that leave at most
+// seg_ana_w (<= 8) warps of 64 beta indices per CTA
+int seg_ana_split(const so3_plan_s* p) {
+  const int warps = p->n / so3::kSegBeta, wmax = std::max(1, std::min(8, p->seg_ana_w));
+  for (int s : {1, 2, 4})
+    if (warps % s == 0 && warps / s <= wmax) return s;
+  return 0;
+}
+
+template <int SPLIT, int WT, int MINB>
+int launch_seg_ana_cfg(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, int W, cudaStream_t st) {
+  constexpr int TB = 8;
+  auto k = so3::dwt_analysis_seg_kernel<16, SPLIT, TB, MINB, WT>;
+  const size_t smem = ((size_t)2 * so3::kSegTabA + (size_t)2 * TB * W * 64) * sizeof(double2) + (size_t)t_knobs.dwt_pad * 1024;
+  SO3_CUDA(set_smem(k, smem));
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
+  k<<<dim3(ncl * SPLIT, SPLIT > 1 ? 1 : p->batch), W * 32, smem, st>>>(a, sp, p->d_ck);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int launch_dwt_seg_ana(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, cudaStream_t st) {
+  const int split = seg_ana_split(p);
+  const int W = split ? p->n / so3::kSegBeta / split : 0;
+  if (split > 1 && (p->batch != 1 || !p->d_pbuf || !p->d_pcnt || p->pbuf_splits < split))
+    return fail(SO3_ERR_INVALID, "segment-parallel split analysis without its plan scratch");
+  switch (split) {
+    case 1: return W <= 4 ? launch_seg_ana_cfg<1, 4, 2>(p, a, ncl, W, st) : launch_seg_ana_cfg<1, 8, 1>(p, a, ncl, W, st);
+    case 2: return W <= 4 ? launch_seg_ana_cfg<2, 4, 2>(p, a, ncl, W, st) : launch_seg_ana_cfg<2, 8, 1>(p, a, ncl, W, st);
+    case 4: return W <= 4 ? launch_seg_ana_cfg<4, 4, 2>(p, a, ncl, W, st) : launch_seg_ana_cfg<4, 8, 1>(p, a, ncl, W, st);
+    default: return fail(SO3_ERR_INVALID, "segment-parallel analysis: no CTA shape for this bandwidth");
+  }
+}
+
+int launch_dwt_seg_syn(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, cudaStream_t st) {
+  const int warps = p->n / so3::kSegBeta;
+  if (warps % 4 == 0) {
+    auto k = so3::dwt_synthesis_seg_kernel<8, 4, 8, 3>;
+    k<<<dim3(ncl * (warps / 4), p->batch), 128, 0, st>>>(a, warps / 4, p->d_ck);
+  } else {
+    auto k = so3::dwt_synthesis_seg_kernel<8, 2, 8, 4>;
+    k<<<dim3(ncl * (warps / 2), p->batch), 64, 0, st>>>(a, warps / 2, p->d_ck);
+  }
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
 template <bool ANALYSIS>
 int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, int64_t c1, cudaStream_t st,
                int64_t chunk_pairs = -1) {
@@ -718,6 +776,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
+  if (seg_applies(p) && (p->dwt_seg & (ANALYSIS ? 2 : 1)) && (!ANALYSIS || seg_ana_split(p) == 1 || p->batch == 1))
+    return ANALYSIS ? launch_dwt_seg_ana(p, a, ncl, st) : launch_dwt_seg_syn(p, a, ncl, st);
   const int syn_jw = p->syn_jw ? p->syn_jw : (p->n >= 512 ? 64 : 0);   // 16 warps per SM (B=512: 32.8 vs 33.7 ms with JW = 128)
   if (p->dwt_variant != SO3_DWT_SIMT && !ANALYSIS && syn_jw && (p->n + syn_jw - 1) / syn_jw <= 16) {
     if (syn_jw == 64) return launch_dwt_mma<64>(false, a, p->n, ncl, p->batch, st);
@@ -821,15 +881,31 @@ int so3_cluster_schedule(int b, int32_t* bases, int32_t* members) {
 
 namespace {
 
-bool split_applies(const so3_plan_s* p) {
-  return p->ana_split && p->batch == 1 && (p->n == 1024 || (p->n == 512 && p->ana_split > 1));
+// partial sets the plan's analysis kernels need in d_pbuf (0: no split kernel applies)
+int split_sets(const so3_plan_s* p) {
+  int sets = 0;
+  if (p->ana_split && p->batch == 1 && (p->n == 1024 || (p->n == 512 && p->ana_split > 1))) sets = 2;
+  if ((p->dwt_seg & 2) && seg_eligible(p) && p->batch == 1) sets = std::max(sets, seg_ana_split(p) > 1 ? seg_ana_split(p) : 0);
+  return sets;
 }
+bool split_applies(const so3_plan_s* p) { return split_sets(p) > 0; }
 
 // Split-analysis scratch: per-half partial sums (2 x rc_entries x 8) and one arrival counter
 // per cluster, allocated together (both or neither) and zeroed synchronously.
 int ensure_split_scratch(so3_plan_s* p) {
-  if (p->d_pbuf && p->d_pcnt) return SO3_OK;
-  const size_t pb = (size_t)2 * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2);
+  const int sets = std::max(2, split_sets(p));
+  if (p->d_pbuf && p->d_pcnt && p->pbuf_splits >= sets) return SO3_OK;
+  if (p->d_pbuf) {   // grow (knob change): the old scratch goes back first
+    cudaDeviceSynchronize();
+    p->bytes -= (int64_t)((size_t)p->pbuf_splits * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2) +
+                          (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned));
+    cudaFree(p->d_pbuf);
+    cudaFree(p->d_pcnt);
+    p->d_pbuf = nullptr;
+    p->d_pcnt = nullptr;
+    p->pbuf_splits = 0;
+  }
+  const size_t pb = (size_t)sets * std::max<long long>(p->rc_entries, 1) * 8 * sizeof(double2);
   const size_t cb = (size_t)std::max<int64_t>(p->nclusters, 1) * sizeof(unsigned);
   double2* buf = nullptr;
   unsigned* cnt = nullptr;
@@ -844,7 +920,41 @@ int ensure_split_scratch(so3_plan_s* p) {
   }
   p->d_pbuf = buf;
   p->d_pcnt = cnt;
+  p->pbuf_splits = sets;
   p->bytes += (int64_t)(pb + cb);
+  return SO3_OK;
+}
+
+// Checkpoint table of the segment-parallel DWT (dwt_seg.cuh): 8 recurrence states per (cluster,
+// beta index), written by one pass of the recurrence.  Not enough memory: the plan keeps the
+// dwt_mma.cuh kernels (dwt_seg off), it does not fail.
+int ensure_checkpoints(so3_plan_s* p) {
+  if (p->d_ck || !p->dwt_seg || !seg_eligible(p) || p->nclusters == 0) return SO3_OK;
+  const size_t bytes = (size_t)p->nclusters * so3::kSegRows * p->n * sizeof(double2);
+  double2* ck = nullptr;
+  if (cudaMalloc((void**)&ck, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    p->dwt_seg = 0;
+    return SO3_OK;
+  }
+  so3::DwtArgs a{};
+  a.B = p->B;
+  a.n = p->n;
+  a.bases = p->d_bases;
+  a.lnorm = p->d_lnorm;
+  a.xv = p->d_xv;
+  a.logcs = p->d_logcs;
+  a.rc = p->d_rc;
+  a.rc_off = p->d_rc_off;
+  so3::dwt_checkpoint_kernel<<<dim3((unsigned)p->nclusters, (p->n + 127) / 128), 128>>>(a, ck);
+  cudaError_t e = cudaGetLastError();
+  e = e ? e : cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    cudaFree(ck);
+    return fail(SO3_ERR_CUDA, std::string("checkpoint table: ") + cudaGetErrorString(e));
+  }
+  p->d_ck = ck;
+  p->bytes += (int64_t)bytes;
   return SO3_OK;
 }
 
@@ -971,6 +1081,7 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   }
   e = e ? e : cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  if (int rc = ensure_checkpoints(p)) return rc;
   if (split_applies(p)) return ensure_split_scratch(p);
   return SO3_OK;
 }
@@ -1155,6 +1266,7 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_rc_off);
   cudaFree(p->d_pbuf);
   cudaFree(p->d_pcnt);
+  cudaFree(p->d_ck);
   cudaFree(p->d_row_global);
   cudaFree(p->d_row_local);
   cudaFree(p->d_grid_stage);
@@ -1181,6 +1293,16 @@ int so3_plan_set_knob(so3_plan_t p, const char* name, int value) {
       if (int rc = ensure_split_scratch(p)) { p->ana_split = old; return rc; }
     }
     return SO3_OK;
+  }
+  if (k == "dwt_seg" || k == "seg_ana_w") {
+    if (k == "seg_ana_w" && value != 4 && value != 8) return fail(SO3_ERR_INVALID, "seg_ana_w must be 4 or 8");
+    int& field = k == "dwt_seg" ? p->dwt_seg : p->seg_ana_w;
+    const int old = field;
+    field = value;
+    int rc = ensure_checkpoints(p);
+    if (!rc && split_applies(p)) rc = ensure_split_scratch(p);
+    if (rc) field = old;
+    return rc;
   }
   if (k == "fft_xb") { p->fft_wide = value; return SO3_OK; }
   if (k == "dwt_batch") { p->dwt_batch = value; return SO3_OK; }
