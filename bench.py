@@ -486,7 +486,9 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
     fused = n in (16, 32, 64)   # one-pass slice FFT (fft2d_slice_tma_kernel: pair-major side by TMA)
     kernel_of = {
         "dwt_analysis": "dwt_analysis_batch_reg_kernel" if (F >= 2 and n <= 64) else "dwt_analysis_mma_cta_kernel",
-        "dwt_synthesis": "dwt_synthesis_batch_kernel" if (F >= 2 and n <= 64) else "dwt_synthesis_mma_kernel",
+        # B a multiple of 64: the segment-parallel synthesis (dwt_seg.cuh) is the library default
+        "dwt_synthesis": "dwt_synthesis_batch_kernel" if (F >= 2 and n <= 64) else
+                         ("dwt_synthesis_seg_kernel" if (n % 128 == 0 and n <= 1024) else "dwt_synthesis_mma_kernel"),
         # launch_fft2d / launch_fft_tma dispatch: one-pass TMA slices at 2B <= 64, TMA-fed passes
         # (rows in -> tensor store; tensor load -> rows out) at 2B in {256, 512, 1024}, else plain
         "fft_analysis": "fft2d_slice_tma_kernel" if fused else

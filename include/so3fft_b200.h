@@ -24,12 +24,15 @@
  *
  * Plans and concurrency: a plan is read-only tables PLUS per-plan scratch (the FFT
  * intermediate, the pair-major spectrum, the split-analysis partial sums and counters,
- * the host-path staging buffers).  Every transform on one plan uses that scratch, so calls
+ * the host-path staging buffers).  For B a multiple of 64 the tables include the checkpoint
+ * table of the segment-parallel DWT (8 recurrence states per cluster and beta index:
+ * 8 x 2B x 16 bytes x B(B+1)/2 clusters, 17.2 GB at B = 512; if that allocation fails the plan
+ * keeps the kernels that need no table).  Every transform on one plan uses that scratch, so calls
  * on ONE plan must be stream-ordered: issue them on one stream, or order the streams
  * yourself (events).  Different plans are independent and may run concurrently on any
  * streams or threads.  (The reference TransformPlan is immutable and may be shared; give
  * each concurrent stream its own plan here.)  No call allocates device memory except
- * so3_plan_create*, so3_plan_set_knob("ana_split") and the first call of a *_host entry
+ * so3_plan_create*, so3_plan_set_knob("ana_split" / "dwt_seg" / "seg_ana_w") and the first call of a *_host entry
  * point, so the device entry points can be captured into a CUDA graph.
  */
 #ifndef SO3FFT_B200_H
@@ -160,7 +163,13 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * "ana_split" (analysis of a cluster over two 4-warp CTAs that combine their halves in a
  * fixed order: 0 = off (one CTA per cluster), 1 = on at 2B = 1024 (default), >= 2 = on at
  * 2B = 512 and 1024; same results to rounding, deterministic; turning it on allocates the
- * partial-sum scratch, 2 x 8 x sum_clusters(B - m) complex128).  Experiment knobs (same results,
+ * partial-sum scratch, 2 x 8 x sum_clusters(B - m) complex128).  "dwt_seg" (segment-parallel
+ * DWT kernels, csrc/dwt_seg.cuh, where B % 64 == 0; bits: 1 = synthesis (default), 2 = analysis
+ * with one CTA per cluster part, 4 = persistent analysis with bulk-copy operand prefetch on
+ * single-device one-function plans; 0 = dwt_mma.cuh kernels; same results to rounding,
+ * deterministic; the analysis variants measured equal to or slower than the default analysis
+ * at the BASELINE sizes), "seg_ana_w" (warps per CTA of those analysis variants, 4 or 8).
+ * Experiment knobs (same results,
  * measured slower or equal): "fft_persist" (> 0: the
  * TMA passes as that many persistent double-buffered CTAs), "fft_pad" / "dwt_pad" (extra KB of
  * shared memory per FFT / MMA DWT CTA), "carveout" (preferred shared-memory carveout of the

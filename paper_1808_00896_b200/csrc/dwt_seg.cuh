@@ -237,6 +237,237 @@ __device__ __forceinline__ void seg_bar_wait(unsigned long long* bar, unsigned p
   } while (!done);
 }
 
+// ---- persistent analysis -------------------------------------------------------------------
+// Above, a CTA lives for one (cluster, beta part): its prologue (three dependent global round
+// trips) and the final combine of a split cluster are exposed, because 236 registers per thread
+// leave one or two CTAs per SM (ncu: DMMA pipe 51 %).  Here one CTA per SM (two for W = 4) walks
+// its share of the clusters, and thread 0 streams the NEXT pass's operands -- 8 checkpoint rows,
+// up to 8 member rows of the spectrum, v_j and the cluster's recurrence table -- into shared
+// memory with 1-D bulk copies (cp.async.bulk, one mbarrier) while the warps work on the current
+// pass, so a prologue is shared-memory reads.  A CTA covers W x 64 beta indices per pass and runs
+// the passes of a cluster (2 at 2B = 1024) back to back: pass 0 leaves its per-degree sums in
+// SplitArgs::pbuf, the last pass adds them to its own in pass order -- same CTA, so no counter,
+// no fence and no combine sweep.  Clusters go to CTAs in snake order over the cost-sorted schedule.
+
+__device__ __forceinline__ unsigned seg_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void seg_bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(seg_smem(dst)),
+               "l"(src), "r"(bytes), "r"(seg_smem(bar))
+               : "memory");
+}
+__device__ __forceinline__ void seg_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(seg_smem(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool seg_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+               : "=r"(done)
+               : "r"(seg_smem(bar)), "r"(parity)
+               : "memory");
+  return done != 0;
+}
+
+constexpr int kSegTabP = 2 * kSegRows * (kSegMaxSL / 2 + 1);   // 528 double2 >= one half at SL <= 64, two at SL <= 32
+constexpr int kSegRawTab = 3 * 512;                             // doubles: a cluster's (alpha, C+, mu) entries
+
+__host__ __device__ inline size_t segp_smem_bytes(int W, int TB) {
+  const size_t RS = (size_t)W * kSegBeta + 4;
+  return 2 * kSegRows * RS * 16 + (size_t)W * kSegBeta * 8 + kSegRawTab * 8 + kSegTabP * 16 + 512 * 8 +
+         (size_t)2 * TB * W * 64 * 16;
+}
+
+// Measured and dropped (B = 512, one B200; this version: see DESIGN.md): a split mbarrier per batch
+// with three partial buffers (36.8 ms: warps still wait for the slowest one, one batch later), and a
+// barrier-free ring of per-step partial tiles reduced kSegLag steps later by all warps (47 ms: the
+// mbarrier polls between the steps keep the compiler from overlapping one step's DFMAs with the
+// next step's DMMAs).
+template <int NB, int TB, int WT, int MINB>
+__global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArgs a, SplitArgs sp, const double2* ck, int ncl,
+                                                                           int halves) {
+  static_assert(4 * NB == kSegBeta, "a warp covers kSegBeta beta indices");
+  constexpr int OPT = 2;   // outputs per thread and batch: TB x 64 outputs over >= TB x 32 threads
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ Member mem[8];
+  __shared__ unsigned long long bar;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, W = blockDim.x >> 5, NT = blockDim.x;
+  const int r = lane >> 2, k = lane & 3;
+  const int WB = W * kSegBeta, RS = WB + 4;   // row stride: +64 bytes, rows r and r+1 of a quarter-warp on distinct banks
+  double2* ckS = reinterpret_cast<double2*>(smraw);   // [8][RS] checkpoint rows of the pass
+  double2* xS = ckS + kSegRows * RS;                  // [8][RS] member rows of the spectrum (mirror ranges for reflecting members)
+  double* vS = reinterpret_cast<double*>(xS + kSegRows * RS);   // [WB]
+  double* rcS = vS + WB;                              // raw table of the cluster
+  double2* rcs = reinterpret_cast<double2*>(rcS + kSegRawTab);   // padded (alpha, C) rows, one or both halves
+  double* mus = reinterpret_cast<double*>(rcs + kSegTabP);       // mu_l of the cluster
+  double2* part = reinterpret_cast<double2*>(mus + 512);          // [2][TB][W][64]
+  const int B = a.B, n = a.n;
+  const int G = gridDim.x, b = blockIdx.x;
+  const double vscale = 8.0 * 3.141592653589793 * (double)B;
+
+  // round i of the snake: cluster i G + b (even i) or i G + G - 1 - b (odd i)
+  auto cluster_of = [&](int i) { return i * G + ((i & 1) ? G - 1 - b : b); };
+  // warp 0: the operands of pass h of cluster c (base m, m') into the stage buffers, one bulk copy
+  // per lane (8 checkpoint rows, 8 member rows, v_j, the recurrence table)
+  auto prefetch = [&](int c, int h, int m, int mp, long long rco) {
+    const int j0 = h * WB;
+    const int nsteps = B - m;
+    const Member M = make_member(m, mp, lane & 7, n);
+    const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, M.valid && lane < 8));
+    const unsigned tabb = h == 0 ? (unsigned)(((nsteps + 1) & ~1) * 24) : 0u;
+    if (lane == 0) seg_expect_tx(&bar, (unsigned)((kSegRows + nvalid) * WB * 16 + WB * 8) + tabb);
+    __syncwarp();
+    if (lane < 8) {
+      seg_bulk_load(ckS + lane * RS, ck + ((long long)c * kSegRows + lane) * n + j0, WB * 16, &bar);
+    } else if (lane < 16) {
+      if (M.valid) seg_bulk_load(xS + (lane - 8) * RS, a.spec + M.row * n + (M.reflect ? n - j0 - WB : j0), WB * 16, &bar);
+    } else if (lane == 16) {
+      seg_bulk_load(vS, a.xv + j0, WB * 8, &bar);
+    } else if (lane == 17 && h == 0) {
+      seg_bulk_load(rcS, a.rc + 3 * rco, tabb, &bar);
+    }
+  };
+
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(seg_smem(&bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int c0 = cluster_of(0);
+  if (c0 >= ncl) return;
+  // (m, m', table offset) of the current cluster and of the next one, loaded a pass ahead
+  int2 base = __ldg(&a.bases[a.cluster0 + c0]);
+  long long rco = __ldg(&a.rc_off[a.cluster0 + c0]);
+  if (warp == 0) prefetch(a.cluster0 + c0, 0, base.x, base.y, rco);
+  unsigned parity = 0;
+  for (int i = 0;; ++i) {
+    const int c = a.cluster0 + cluster_of(i);
+    const int cn = cluster_of(i + 1);
+    int2 base_n = make_int2(0, 0);
+    long long rco_n = 0;
+    if (cn < ncl) {
+      base_n = __ldg(&a.bases[a.cluster0 + cn]);
+      rco_n = __ldg(&a.rc_off[a.cluster0 + cn]);
+    }
+    const int m = base.x, mp = base.y;
+    const int nsteps = B - m, SL = seg_len(nsteps), SLP = SL | 1;
+    for (int h = 0; h < halves; ++h) {
+      while (!seg_try_wait(&bar, parity)) {}
+      parity ^= 1;
+      const int j0 = h * WB;
+      // padded table rows and mu_l from the raw table (which stays until the next cluster's pass 0 arrives)
+      if (h == 0 && t < 8) mem[t] = make_member(m, mp, t, n);
+      const bool both = halves == 1;         // the CTA spans [0, pi): both table halves
+      const bool upper_pass = 2 * j0 >= n;   // halves > 1: the pass lies in one half
+      for (int idx = t; idx < kSegRows * SL; idx += NT) {
+        const int rr = idx / SL, tt = idx - rr * SL;
+        double al = 0.0, cp = 0.0;
+        if (idx < nsteps) {
+          al = rcS[3 * idx];
+          cp = rcS[3 * idx + 1];
+          if (h == 0) mus[idx] = rcS[3 * idx + 2];
+        }
+        if (both) {
+          rcs[rr * SLP + tt] = make_double2(al, cp);
+          rcs[kSegRows * SLP + rr * SLP + tt] = make_double2(al, fma(-2.0, al, cp));
+        } else {
+          rcs[rr * SLP + tt] = make_double2(al, upper_pass ? fma(-2.0, al, cp) : cp);
+        }
+      }
+      // operands of this warp from the stage buffers
+      const int jl0 = warp * kSegBeta;
+      double cur[NB], prev[NB], v[NB], xr[NB], xi[NB];
+      {
+        const Member M = make_member(m, mp, r, n);
+        const double2* cr = ckS + r * RS + jl0 + k;
+        const double2* xrow = xS + r * RS + (M.reflect ? WB - 1 - jl0 - k : jl0 + k);
+        const int xstep = M.reflect ? -4 : 4;
+#pragma unroll
+        for (int g = 0; g < NB; ++g) {
+          const double2 s = cr[4 * g];
+          cur[g] = s.x;
+          prev[g] = s.y;
+          v[g] = vS[jl0 + 4 * g + k];
+          double2 z = make_double2(0.0, 0.0);
+          if (M.valid) z = xrow[xstep * g];
+          xr[g] = z.x;
+          xi[g] = z.y;
+        }
+      }
+      __syncthreads();   // the stage buffers are free; the padded table, mu and the members are visible
+      if (warp == 0) {   // next pass: the other half of this cluster, or the next cluster
+        if (h + 1 < halves) prefetch(c, h + 1, m, mp, rco);
+        else if (cn < ncl) prefetch(a.cluster0 + cn, 0, base_n.x, base_n.y, rco_n);
+      }
+      const double2* rw = rcs + ((both && 2 * (j0 + jl0) >= n) ? kSegRows * SLP : 0) + r * SLP;
+      const bool last = h + 1 == halves;
+      int buf = 0;
+      for (int t0 = 0; t0 < SL; t0 += TB, buf ^= 1) {
+        const int nt = min(TB, SL - t0);
+        // pass 0's sums of this thread's outputs of the batch go out before the batch's math
+        double2 p0[OPT];
+#pragma unroll
+        for (int q = 0; q < OPT; ++q) {
+          const int idx = t + q * NT, tb = idx >> 6, o = idx & 63;
+          const int mm = 2 * (o & 3) + (o >> 5), ii = ((o >> 2) & 7) * SL + t0 + tb;
+          p0[q] = make_double2(0.0, 0.0);
+          if (h > 0 && idx < nt * 64 && ii < nsteps) p0[q] = __ldcg(&sp.pbuf[(rco + ii) * 8 + mm]);
+        }
+        double2* pw = part + ((size_t)buf * TB * W + warp) * 64 + lane;
+#pragma unroll 2
+        for (int tb = 0; tb < nt; ++tb) {
+          const double2 k2 = rw[t0 + tb];
+          double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+          for (int g = 0; g < NB; ++g) {
+            dmma884(a0, a1, cur[g], xr[g]);
+            dmma884(b0, b1, cur[g], xi[g]);
+            const double nx = fma(fma(k2.x, v[g], k2.y), cur[g], -prev[g]);
+            prev[g] = cur[g];
+            cur[g] = nx;
+          }
+          // lane (r, k): segment r, members 2k (a0, b0) and 2k + 1 (a1, b1) as (re, im)
+          pw[(size_t)tb * W * 64] = make_double2(a0, b0);
+          pw[(size_t)tb * W * 64 + 32] = make_double2(a1, b1);
+        }
+        __syncthreads();   // every warp's partials of these nt steps are visible
+#pragma unroll
+        for (int q = 0; q < OPT; ++q) {
+          const int idx = t + q * NT;
+          if (idx >= nt * 64) continue;
+          const int tb = idx >> 6, o = idx & 63;
+          const int mm = 2 * (o & 3) + (o >> 5), rr = (o >> 2) & 7;
+          const int ii = rr * SL + t0 + tb;   // degree l = m + ii
+          const double2* pb = part + (size_t)(buf * TB + tb) * W * 64 + o;
+          double2 vv[WT];
+#pragma unroll
+          for (int w = 0; w < WT; ++w) vv[w] = w < W ? pb[w * 64] : make_double2(0.0, 0.0);
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int w = 0; w < WT; ++w) {   // fixed order
+            re += vv[w].x;
+            im += vv[w].y;
+          }
+          const Member M = mem[mm];
+          if (ii >= nsteps || !M.valid) continue;
+          if (!last) {   // passes accumulate in pass order
+            sp.pbuf[(rco + ii) * 8 + mm] = make_double2(p0[q].x + re, p0[q].y + im);
+          } else {
+            const int l = m + ii;
+            double sc = (2.0 * l + 1.0) / vscale * mus[ii];   // v_l * mu_l
+            if ((M.sl * l + M.par0) & 1) sc = -sc;
+            a.coef[coeff_slot(l, M.pm, M.pmp)] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
+          }
+        }
+        // the next TB steps write the other buffer; this one is rewritten only after the next
+        // __syncthreads, which every reader has passed
+      }
+      __syncthreads();   // the last reducers are done with mem / mus / the table before the next pass rewrites them
+    }
+    if (cn >= ncl) break;
+    base = base_n;
+    rco = rco_n;
+  }
+}
+
 // Synthesis.  Grid (clusters x split, batch); WPC warps per CTA, each over 8 NB beta indices
 // (NB row groups); split x WPC x 8 NB = 2B.  Lane (r, k): beta row r of each group, degree segment
 // k of 4 (length SL4 = 2 SL).

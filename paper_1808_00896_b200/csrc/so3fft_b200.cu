@@ -209,7 +209,7 @@ struct so3_plan_s {
   double2* d_pbuf = nullptr;      // split analysis: per-half partial sums, 2 x rc_entries x 8
   unsigned* d_pcnt = nullptr;     // split analysis: per-cluster arrival counters
   // segment-parallel DWT (dwt_seg.cuh): checkpoint table [cluster][8][2B] of recurrence states
-  int dwt_seg = 1;                // knob, bits: 1 = segment-parallel synthesis, 2 = analysis (where B % 64 == 0)
+  int dwt_seg = 1;                // knob, bits: 1 = segment-parallel synthesis, 2 = analysis, 4 = persistent analysis (B % 64 == 0)
   int seg_ana_w = 8;              // knob: most warps per analysis CTA (8: one CTA per SM; 4: two)
   double2* d_ck = nullptr;
   int pbuf_splits = 0;            // partial sets d_pbuf holds
@@ -735,6 +735,46 @@ int launch_dwt_seg_ana(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl,
   }
 }
 
+// Persistent segment-parallel analysis (single-device plans, one function): CTAs of W <= 8 warps
+// over W x 64 beta indices, `halves` passes per cluster, as many CTAs as fit the device.
+template <int WT, int MINB, int TB>
+int launch_seg_ana_persist(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, int W, int halves, cudaStream_t st) {
+  auto k = so3::dwt_analysis_segp_kernel<16, TB, WT, MINB>;
+  const size_t smem = so3::segp_smem_bytes(W, TB) + (size_t)t_knobs.dwt_pad * 1024;
+  SO3_CUDA(set_smem(k, smem));
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, size_t>, int> ctas;   // (device, threads, smem) -> resident CTAs per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int grid = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_tuple(dev, W * 32 + 4096 * WT, smem);
+    auto it = ctas.find(key);
+    if (it == ctas.end()) {
+      int per_sm = 0, sms = 0;
+      SO3_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, W * 32, smem));
+      SO3_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      it = ctas.emplace(key, std::max(1, per_sm) * sms).first;
+    }
+    grid = it->second;
+  }
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
+  k<<<std::min<unsigned>(ncl, (unsigned)grid), W * 32, smem, st>>>(a, sp, p->d_ck, (int)ncl, halves);
+  SO3_CUDA(cudaGetLastError());
+  return SO3_OK;
+}
+
+int launch_dwt_seg_anap(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, cudaStream_t st) {
+  const int warps = p->n / so3::kSegBeta;
+  int halves = warps > 8 ? 2 : 1;
+  if (p->seg_ana_w == 4 && warps % 4 == 0) halves = warps / 4;   // two 4-warp CTAs per SM
+  if (warps % halves) return fail(SO3_ERR_INVALID, "persistent analysis: odd warp count");
+  const int W = warps / halves;
+  if (halves > 1 && !p->d_pbuf) return fail(SO3_ERR_INVALID, "persistent analysis without its plan scratch");
+  return W <= 4 ? launch_seg_ana_persist<4, 2, 2>(p, a, ncl, W, halves, st) : launch_seg_ana_persist<8, 1, 4>(p, a, ncl, W, halves, st);
+}
+
 int launch_dwt_seg_syn(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, cudaStream_t st) {
   const int warps = p->n / so3::kSegBeta;
   if (warps % 4 == 0) {
@@ -776,6 +816,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   const unsigned ncl = (unsigned)(c1 - c0);
   if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
     return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
+  if (ANALYSIS && seg_applies(p) && (p->dwt_seg & 4) && !p->sharded && p->batch == 1 && p->n / so3::kSegBeta >= 4)
+    return launch_dwt_seg_anap(p, a, ncl, st);
   if (seg_applies(p) && (p->dwt_seg & (ANALYSIS ? 2 : 1)) && (!ANALYSIS || seg_ana_split(p) == 1 || p->batch == 1))
     return ANALYSIS ? launch_dwt_seg_ana(p, a, ncl, st) : launch_dwt_seg_syn(p, a, ncl, st);
   const int syn_jw = p->syn_jw ? p->syn_jw : (p->n >= 512 ? 64 : 0);   // 16 warps per SM (B=512: 32.8 vs 33.7 ms with JW = 128)
@@ -886,6 +928,7 @@ int split_sets(const so3_plan_s* p) {
   int sets = 0;
   if (p->ana_split && p->batch == 1 && (p->n == 1024 || (p->n == 512 && p->ana_split > 1))) sets = 2;
   if ((p->dwt_seg & 2) && seg_eligible(p) && p->batch == 1) sets = std::max(sets, seg_ana_split(p) > 1 ? seg_ana_split(p) : 0);
+  if ((p->dwt_seg & 4) && seg_eligible(p) && p->batch == 1 && !p->sharded && p->n / so3::kSegBeta > 4) sets = std::max(sets, 1);
   return sets;
 }
 bool split_applies(const so3_plan_s* p) { return split_sets(p) > 0; }
@@ -893,7 +936,7 @@ bool split_applies(const so3_plan_s* p) { return split_sets(p) > 0; }
 // Split-analysis scratch: per-half partial sums (2 x rc_entries x 8) and one arrival counter
 // per cluster, allocated together (both or neither) and zeroed synchronously.
 int ensure_split_scratch(so3_plan_s* p) {
-  const int sets = std::max(2, split_sets(p));
+  const int sets = split_sets(p);
   if (p->d_pbuf && p->d_pcnt && p->pbuf_splits >= sets) return SO3_OK;
   if (p->d_pbuf) {   // grow (knob change): the old scratch goes back first
     cudaDeviceSynchronize();
@@ -1029,7 +1072,9 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   long long rc_entries = 0;
   for (size_t i = 0; i < cl.size(); ++i) {
     rc_off[i] = rc_entries;
-    rc_entries += b - cl[i].m;   // one (alpha, beta, mu) per degree
+    // one (alpha, C+, mu) per degree; an even count, so every cluster's table starts 16-byte
+    // aligned and is a multiple of 16 bytes (1-D bulk copies, dwt_seg.cuh)
+    rc_entries += (b - cl[i].m + 1) & ~1;
   }
   p->rc_entries = rc_entries;
   rc_entries = std::max(rc_entries, 1LL);

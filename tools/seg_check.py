@@ -6,6 +6,9 @@ import numpy as np, torch
 import paper_1808_00896_b200 as so3
 
 
+SEG = int(os.environ.get('SEG', '3'))
+
+
 def timed(fn, reps=5):
     fn(); torch.cuda.synchronize()
     out = []
@@ -27,11 +30,11 @@ for b in [int(x) for x in (sys.argv[1:] or [64, 128, 256])]:
     out = {s: torch.zeros(C, dtype=torch.complex128, device="cuda") for s in (0, 1)}
     res = {"B": b, "plan_GB": round(plan.device_bytes / 1e9, 2) if hasattr(plan, "device_bytes") else None}
     for s in (0, 1):
-        plan.set_knob("dwt_seg", 3 * s)
+        plan.set_knob("dwt_seg", SEG * s)
         res[f"syn_ms_seg{s}"] = round(timed(lambda: so3.dwt_synthesis(plan, coef, spec[s])), 4)
     # the analysis of the SAME spectrum (the old kernels' synthesis) under both settings
     for s in (0, 1):
-        plan.set_knob("dwt_seg", 3 * s)
+        plan.set_knob("dwt_seg", SEG * s)
         res[f"ana_ms_seg{s}"] = round(timed(lambda: so3.dwt_analysis(plan, spec[0], out[s])), 4)
     d_syn = (spec[1] - spec[0]).abs().max().item() / spec[0].abs().max().item()
     d_ana = (out[1] - out[0]).abs().max().item() / out[0].abs().max().item()
