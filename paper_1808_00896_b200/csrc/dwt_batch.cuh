@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
   }
   const bool two_tiles = mem[4].valid;
   const double vscale = 8.0 * 3.141592653589793 * (double)B;
+  const double rvscale = 1.0 / vscale;   // one division per thread: a DDIV per output kept the FP64 pipe busy in the reductions
   double2* coef = a.coef + (long long)(f0 + fl) * a.coef_fstride;
 
   for (int l0 = m; l0 < B; l0 += 32) {
@@ -136,7 +137,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
     for (int mt = 0; mt < 4; ++mt) {
       const int l = l0 + 8 * mt + g;
       if (mt >= mtn || l >= B) continue;
-      const double vmu = (2.0 * l + 1.0) / vscale * __ldg(&rct[3 * (l - m) + 2]);   // v_l * mu_l
+      const double vmu = (2.0 * l + 1.0) * rvscale * __ldg(&rct[3 * (l - m) + 2]);   // v_l * mu_l
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const Member M = mem[4 * nt + tq];

@@ -137,6 +137,8 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_seg_kernel(DwtArgs
   }
 
   const double vscale = 8.0 * 3.141592653589793 * (double)B;
+
+  const double rvscale = 1.0 / vscale;   // one division per thread, not one per output
   int buf = 0;
   for (int t0 = 0; t0 < SL; t0 += TB, buf ^= 1) {
     const int nt = min(TB, SL - t0);
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_seg_kernel(DwtArgs
         sp.pbuf[half * sp.pstride + (rco + i) * 8 + mm] = make_double2(re, im);
       } else {
         const int l = m + i;
-        double sc = (2.0 * l + 1.0) / vscale * __ldg(&rct[3 * i + 2]);   // v_l * mu_l
+        double sc = (2.0 * l + 1.0) * rvscale * __ldg(&rct[3 * i + 2]);   // v_l * mu_l
         if ((M.sl * l + M.par0) & 1) sc = -sc;
         a.coef[(long long)f * a.coef_fstride + coeff_slot(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
       }
@@ -209,7 +211,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_seg_kernel(DwtArgs
         re += ph.x;
         im += ph.y;
       }
-      double sc = (2.0 * l + 1.0) / vscale * __ldg(&rct[3 * i + 2]);
+      double sc = (2.0 * l + 1.0) * rvscale * __ldg(&rct[3 * i + 2]);
       if ((M.sl * l + M.par0) & 1) sc = -sc;
       a.coef[(long long)f * a.coef_fstride + coeff_slot(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
     }
@@ -302,6 +304,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
   const int B = a.B, n = a.n;
   const int G = gridDim.x, b = blockIdx.x;
   const double vscale = 8.0 * 3.141592653589793 * (double)B;
+  const double rvscale = 1.0 / vscale;   // one division per thread, not one per output
 
   // round i of the snake: cluster i G + b (even i) or i G + G - 1 - b (odd i)
   auto cluster_of = [&](int i) { return i * G + ((i & 1) ? G - 1 - b : b); };
@@ -452,7 +455,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
             sp.pbuf[(rco + ii) * 8 + mm] = make_double2(p0[q].x + re, p0[q].y + im);
           } else {
             const int l = m + ii;
-            double sc = (2.0 * l + 1.0) / vscale * mus[ii];   // v_l * mu_l
+            double sc = (2.0 * l + 1.0) * rvscale * mus[ii];   // v_l * mu_l
             if ((M.sl * l + M.par0) & 1) sc = -sc;
             a.coef[coeff_slot(l, M.pm, M.pmp)] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
           }

@@ -9,7 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 b = int(sys.argv[1])
-paths = [sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else
+paths = sys.argv[2:] if os.environ.get("AB_ONLY") else [sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else
          os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1808_00896_b200",
                       "libso3fft_b200.so")]
 n = 2 * b
@@ -28,6 +28,9 @@ for p in paths:
     lib.so3_cluster_count.restype = ctypes.c_int64
     h = ctypes.c_void_p()
     assert lib.so3_plan_create(b, 1, ctypes.byref(h)) == 0
+    for kv in filter(None, os.environ.get("SO3_KNOBS", "").split(",")):   # per-plan knobs for every library
+        k, v = kv.split("=")
+        assert lib.so3_plan_set_knob(h, k.encode(), int(v)) == 0, kv
     libs.append(lib)
     plans.append(h)
 ncl = libs[0].so3_cluster_count(b)
