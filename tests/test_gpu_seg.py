@@ -107,3 +107,23 @@ def test_seg_knob_off_without_checkpoints_and_ineligible_bandwidths():
     b = 64
     plan = so3.make_plan(b)
     assert plan.device_bytes >= (b * (b + 1) // 2) * 8 * 2 * b * 16
+
+
+def test_seg_synthesis_batched_plan_matches_single_function_plans():
+    """A batched plan at B = 64 (beyond the dense-contraction kernels' 2B <= 64) runs the segment
+    synthesis once per function (grid.y): bit-identical to one-function plans."""
+    b, f = 64, 3
+    n, C = 2 * b, O.n_coeffs(b)
+    rng = np.random.default_rng(7)
+    c = rng.standard_normal(f * C) + 1j * rng.standard_normal(f * C)
+    pb = so3.make_plan(b, batch=f)
+    spec_b = torch.zeros(f * n ** 3, dtype=torch.complex128, device="cuda")
+    so3.dwt_synthesis(pb, torch.from_numpy(c).cuda(), spec_b)
+    p1 = so3.make_plan(b)
+    for i in range(f):
+        s1 = torch.zeros(n ** 3, dtype=torch.complex128, device="cuda")
+        so3.dwt_synthesis(p1, torch.from_numpy(c[i * C:(i + 1) * C].copy()).cuda(), s1)
+        assert torch.equal(s1, spec_b[i * n ** 3:(i + 1) * n ** 3])
+    g = so3.ifsoft_batch(c, pb)
+    back = so3.fsoft_batch(g, pb)
+    assert np.abs(np.asarray(back).reshape(-1) - c).max() < 1e-11
