@@ -1139,6 +1139,10 @@ so3_plan_s* new_plan(int b, int batch) {
   p->ncoef = so3_coeff_count(b);
   p->ngrid = so3_grid_count(b);
   p->J = p->n;
+  // 2B / 64 in {10, 12, 14} (B = 320, 384, 448): the dwt_mma.cuh analysis has no split shape for these
+  // sizes (its one-CTA form needs <= 8 warps of 128 beta and runs 10.0 ms at B = 320); the
+  // persistent segment analysis covers them with two passes per cluster (8.7 ms)
+  if (b % 64 == 0 && b > 256 && b < 512 && batch == 1) p->dwt_seg |= 4;
   cudaGetDevice(&p->device);
   return p;
 }

@@ -127,3 +127,28 @@ def test_seg_synthesis_batched_plan_matches_single_function_plans():
     g = so3.ifsoft_batch(c, pb)
     back = so3.fsoft_batch(g, pb)
     assert np.abs(np.asarray(back).reshape(-1) - c).max() < 1e-11
+
+
+def test_default_analysis_at_b320_is_the_persistent_segment_kernel():
+    """B = 320 (2B / 64 = 10 warps): the plan's default analysis is the persistent segment kernel
+    (two passes per cluster through the plan scratch): equal to the knob-selected kernel, within
+    rounding of the dwt_mma.cuh analysis, and the whole round trip recovers the coefficients."""
+    b = 320
+    plan = so3.make_plan(b)
+    c = seeded(b)
+    cd = torch.from_numpy(c).cuda()
+    spec = torch.zeros((2 * b) ** 3, dtype=torch.complex128, device="cuda")
+    so3.dwt_synthesis(plan, cd, spec)
+    out_default = torch.zeros_like(cd)
+    so3.dwt_analysis(plan, spec, out_default)
+    plan.set_knob("dwt_seg", 1)                      # dwt_mma.cuh analysis
+    out_mma = torch.zeros_like(cd)
+    so3.dwt_analysis(plan, spec, out_mma)
+    plan.set_knob("dwt_seg", 5)
+    out_p = torch.zeros_like(cd)
+    so3.dwt_analysis(plan, spec, out_p)
+    assert torch.equal(out_default, out_p)          # the default IS the persistent kernel
+    assert (out_p - out_mma).abs().max().item() <= 1e-14 * out_mma.abs().max().item()
+    g = so3.ifsoft_sequential(so3.So3Coefficients(b, cd), plan)
+    back = so3.fsoft_sequential(g, plan).data
+    assert (back - cd).abs().max().item() < 1e-11
