@@ -559,8 +559,9 @@ def run_gpu_arm(args, rank: int, world: int, dist) -> None:
         "fft_synthesis": "fft2d_slice_tma_kernel" if fused else
                          ("fft_pass_tload_kernel x2" if n in (256, 512, 1024) else "fft_pass_kernel x2"),
     }
-    if kernel_of["dwt_analysis"] == "dwt_analysis_mma_cta_kernel" and n == 1024:
-        kernel_of["dwt_analysis"] += " (split over two CTAs per cluster)"
+    if kernel_of["dwt_analysis"] == "dwt_analysis_mma_cta_kernel" and n % 128 == 0 and 512 < n <= 1024:
+        # library default at B = 320 .. 512 (dwt_seg bit 4): persistent CTAs, two passes per cluster
+        kernel_of["dwt_analysis"] = "dwt_analysis_segp_kernel (persistent, segment-parallel)"
     stages = {}
     for nm in stage_names:
         ms = stage_ms[nm]

@@ -283,15 +283,20 @@ __host__ __device__ inline size_t segp_smem_bytes(int W, int TB) {
 // barrier-free ring of per-step partial tiles reduced kSegLag steps later by all warps (47 ms: the
 // mbarrier polls between the steps keep the compiler from overlapping one step's DFMAs with the
 // next step's DMMAs).
-template <int NB, int TB, int WT, int MINB>
+// FULLW: the CTA has exactly WT warps (the common shapes: 8 warps at B = 256 and 512, 4 at B = 128);
+// the reduction then has compile-time trip counts and no warp-count selects (it was ~400 SASS
+// instructions per batch and thread, issue-bound: ncu, 9 % of the kernel's warp time).
+template <int NB, int TB, int WT, int MINB, bool FULLW = false>
 __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArgs a, SplitArgs sp, const double2* ck, int ncl,
                                                                            int halves) {
   static_assert(4 * NB == kSegBeta, "a warp covers kSegBeta beta indices");
-  constexpr int OPT = 2;   // outputs per thread and batch: TB x 64 outputs over >= TB x 32 threads
+  // outputs per thread and batch: TB x 64 outputs over the CTA's threads (>= 128 when not FULLW)
+  constexpr int OPT = FULLW ? (TB * 64 + WT * 32 - 1) / (WT * 32) : 2;
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ Member mem[8];
   __shared__ unsigned long long bar;
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, W = blockDim.x >> 5, NT = blockDim.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int W = FULLW ? WT : (int)(blockDim.x >> 5), NT = FULLW ? WT * 32 : (int)blockDim.x;
   const int r = lane >> 2, k = lane & 3;
   const int WB = W * kSegBeta, RS = WB + 4;   // row stride: +64 bytes, rows r and r+1 of a quarter-warp on distinct banks
   double2* ckS = reinterpret_cast<double2*>(smraw);   // [8][RS] checkpoint rows of the pass
@@ -360,19 +365,21 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
       if (h == 0 && t < 8) mem[t] = make_member(m, mp, t, n);
       const bool both = halves == 1;         // the CTA spans [0, pi): both table halves
       const bool upper_pass = 2 * j0 >= n;   // halves > 1: the pass lies in one half
-      for (int idx = t; idx < kSegRows * SL; idx += NT) {
-        const int rr = idx / SL, tt = idx - rr * SL;
-        double al = 0.0, cp = 0.0;
-        if (idx < nsteps) {
-          al = rcS[3 * idx];
-          cp = rcS[3 * idx + 1];
-          if (h == 0) mus[idx] = rcS[3 * idx + 2];
-        }
-        if (both) {
-          rcs[rr * SLP + tt] = make_double2(al, cp);
-          rcs[kSegRows * SLP + rr * SLP + tt] = make_double2(al, fma(-2.0, al, cp));
-        } else {
-          rcs[rr * SLP + tt] = make_double2(al, upper_pass ? fma(-2.0, al, cp) : cp);
+      for (int rr = warp; rr < kSegRows; rr += W) {   // one table row per warp: no division per entry
+        for (int tt = lane; tt < SL; tt += 32) {
+          const int idx = rr * SL + tt;
+          double al = 0.0, cp = 0.0;
+          if (idx < nsteps) {
+            al = rcS[3 * idx];
+            cp = rcS[3 * idx + 1];
+            if (h == 0) mus[idx] = rcS[3 * idx + 2];
+          }
+          if (both) {
+            rcs[rr * SLP + tt] = make_double2(al, cp);
+            rcs[kSegRows * SLP + rr * SLP + tt] = make_double2(al, fma(-2.0, al, cp));
+          } else {
+            rcs[rr * SLP + tt] = make_double2(al, upper_pass ? fma(-2.0, al, cp) : cp);
+          }
         }
       }
       // operands of this warp from the stage buffers
@@ -402,6 +409,25 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
       }
       const double2* rw = rcs + ((both && 2 * (j0 + jl0) >= n) ? kSegRows * SLP : 0) + r * SLP;
       const bool last = h + 1 == halves;
+      // Per-pass constants of this thread's outputs: output q is entry o_q of step tb_q of every batch
+      // (NT is a multiple of 64 for even W; odd W recomputes nothing either: idx = t + q NT is fixed).
+      int o_tb[OPT], o_mm[OPT], o_i0[OPT], o_neg[OPT];
+      bool o_ok[OPT];
+      long long o_pm[OPT];
+      const double2* o_pb[OPT];
+#pragma unroll
+      for (int q = 0; q < OPT; ++q) {
+        const int idx = t + q * NT, tb = idx >> 6, o = idx & 63;
+        const int mm = 2 * (o & 3) + (o >> 5);
+        const Member M = mem[mm];
+        o_tb[q] = tb;
+        o_mm[q] = mm;
+        o_i0[q] = ((o >> 2) & 7) * SL + tb;           // + t0 = degree index of the output
+        o_ok[q] = tb < TB && M.valid;
+        o_neg[q] = M.sl | (M.par0 << 1);               // sign (-1)^(sl l + par0)
+        o_pm[q] = ((long long)M.pm << 32) | (unsigned)M.pmp;
+        o_pb[q] = part + (size_t)tb * W * 64 + o;
+      }
       int buf = 0;
       for (int t0 = 0; t0 < SL; t0 += TB, buf ^= 1) {
         const int nt = min(TB, SL - t0);
@@ -409,10 +435,11 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
         double2 p0[OPT];
 #pragma unroll
         for (int q = 0; q < OPT; ++q) {
-          const int idx = t + q * NT, tb = idx >> 6, o = idx & 63;
-          const int mm = 2 * (o & 3) + (o >> 5), ii = ((o >> 2) & 7) * SL + t0 + tb;
+          const int ii = o_i0[q] + t0;
           p0[q] = make_double2(0.0, 0.0);
-          if (h > 0 && idx < nt * 64 && ii < nsteps) p0[q] = __ldcg(&sp.pbuf[(rco + ii) * 8 + mm]);
+          // volatile: the load leaves BEFORE the batch's DMMAs (ptxas may otherwise sink it to its use)
+          if (h > 0 && o_ok[q] && o_tb[q] < nt && ii < nsteps)
+            asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(p0[q].x), "=d"(p0[q].y) : "l"(&sp.pbuf[(rco + ii) * 8 + o_mm[q]]) : "memory");
         }
         double2* pw = part + ((size_t)buf * TB * W + warp) * 64 + lane;
 #pragma unroll 2
@@ -434,30 +461,25 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
         __syncthreads();   // every warp's partials of these nt steps are visible
 #pragma unroll
         for (int q = 0; q < OPT; ++q) {
-          const int idx = t + q * NT;
-          if (idx >= nt * 64) continue;
-          const int tb = idx >> 6, o = idx & 63;
-          const int mm = 2 * (o & 3) + (o >> 5), rr = (o >> 2) & 7;
-          const int ii = rr * SL + t0 + tb;   // degree l = m + ii
-          const double2* pb = part + (size_t)(buf * TB + tb) * W * 64 + o;
+          const int ii = o_i0[q] + t0;   // degree l = m + ii
+          if (!o_ok[q] || o_tb[q] >= nt || ii >= nsteps) continue;
+          const double2* pb = o_pb[q] + (size_t)buf * TB * W * 64;
           double2 vv[WT];
 #pragma unroll
-          for (int w = 0; w < WT; ++w) vv[w] = w < W ? pb[w * 64] : make_double2(0.0, 0.0);
+          for (int w = 0; w < WT; ++w) vv[w] = (FULLW || w < W) ? pb[w * 64] : make_double2(0.0, 0.0);
           double re = 0.0, im = 0.0;
 #pragma unroll
           for (int w = 0; w < WT; ++w) {   // fixed order
             re += vv[w].x;
             im += vv[w].y;
           }
-          const Member M = mem[mm];
-          if (ii >= nsteps || !M.valid) continue;
           if (!last) {   // passes accumulate in pass order
-            sp.pbuf[(rco + ii) * 8 + mm] = make_double2(p0[q].x + re, p0[q].y + im);
+            sp.pbuf[(rco + ii) * 8 + o_mm[q]] = make_double2(p0[q].x + re, p0[q].y + im);
           } else {
             const int l = m + ii;
             double sc = (2.0 * l + 1.0) * rvscale * mus[ii];   // v_l * mu_l
-            if ((M.sl * l + M.par0) & 1) sc = -sc;
-            a.coef[coeff_slot(l, M.pm, M.pmp)] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
+            if (((o_neg[q] & 1) * l + (o_neg[q] >> 1)) & 1) sc = -sc;
+            a.coef[coeff_slot(l, (int)(o_pm[q] >> 32), (int)o_pm[q])] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
           }
         }
         // the next TB steps write the other buffer; this one is rewritten only after the next

@@ -739,7 +739,7 @@ int launch_dwt_seg_ana(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl,
 // over W x 64 beta indices, `halves` passes per cluster, as many CTAs as fit the device.
 template <int WT, int MINB, int TB>
 int launch_seg_ana_persist(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl, int W, int halves, cudaStream_t st) {
-  auto k = so3::dwt_analysis_segp_kernel<16, TB, WT, MINB>;
+  auto k = W == WT ? so3::dwt_analysis_segp_kernel<16, TB, WT, MINB, true> : so3::dwt_analysis_segp_kernel<16, TB, WT, MINB, false>;
   const size_t smem = so3::segp_smem_bytes(W, TB) + (size_t)t_knobs.dwt_pad * 1024;
   SO3_CUDA(set_smem(k, smem));
   static std::mutex mu;
@@ -749,7 +749,7 @@ int launch_seg_ana_persist(const so3_plan_s* p, const so3::DwtArgs& a, unsigned 
   int grid = 0;
   {
     std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_tuple(dev, W * 32 + 4096 * WT, smem);
+    auto key = std::make_tuple(dev, W * 32 + 4096 * WT, smem);   // (W, WT) also selects the FULLW instantiation
     auto it = ctas.find(key);
     if (it == ctas.end()) {
       int per_sm = 0, sms = 0;
@@ -1139,10 +1139,10 @@ so3_plan_s* new_plan(int b, int batch) {
   p->ncoef = so3_coeff_count(b);
   p->ngrid = so3_grid_count(b);
   p->J = p->n;
-  // 2B / 64 in {10, 12, 14} (B = 320, 384, 448): the dwt_mma.cuh analysis has no split shape for these
-  // sizes (its one-CTA form needs <= 8 warps of 128 beta and runs 10.0 ms at B = 320); the
-  // persistent segment analysis covers them with two passes per cluster (8.7 ms)
-  if (b % 64 == 0 && b > 256 && b < 512 && batch == 1) p->dwt_seg |= 4;
+  // 2B / 64 > 8 (B = 320 .. 512): the persistent segment analysis (two passes per cluster) is the
+  // default: 31.9 ms at B = 512 against 33.9 ms for the split dwt_mma.cuh analysis, 9.2 against
+  // 10.0 ms at B = 320 (no split shape there); at B <= 256 the dwt_mma.cuh analysis is as fast
+  if (b % 64 == 0 && b > 256 && b <= 512 && batch == 1) p->dwt_seg |= 4;
   cudaGetDevice(&p->device);
   return p;
 }

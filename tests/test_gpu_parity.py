@@ -615,6 +615,9 @@ def test_split_analysis_matches_one_cta_reduction_b512():
     spec = torch.randn(n ** 3, dtype=torch.complex128, device="cuda", generator=gen)
     plan = plan_for(b)
     C = so3.coeff_count(b)
+    default = torch.zeros(C, dtype=torch.complex128, device="cuda")
+    so3.dwt_analysis(plan, spec, default)          # the plan's default at B = 512: persistent segment analysis
+    plan.set_knob("dwt_seg", 1)                    # dwt_mma.cuh analysis kernels
     outs = []
     for split in (0, 1, 1):
         plan.set_knob("ana_split", split)
@@ -624,6 +627,7 @@ def test_split_analysis_matches_one_cta_reduction_b512():
     torch.cuda.synchronize()
     assert (outs[1] - outs[0]).abs().max().item() <= 1e-14 * outs[0].abs().max().item()
     assert torch.equal(outs[1], outs[2])
+    assert (default - outs[0]).abs().max().item() <= 1e-14 * outs[0].abs().max().item()
 
 
 # ---------------------------------------------------------------- wigner.py utilities (reference surface)

@@ -72,13 +72,22 @@ def test_sharded_equals_single_gpu_bitwise(b, world, chunks):
     C = so3.coeff_count(b)
     coeffs = torch.from_numpy(rng.standard_normal(C) + 1j * rng.standard_normal(C)).cuda()
     plan = so3.make_plan(b)
+    dflt_f = None
+    if b % 64 == 0 and b > 256:
+        # B = 320 .. 512: the single-device default analysis is the persistent segment kernel, which
+        # sums beta in 64-index warp groups; sharded plans keep the dwt_mma.cuh analysis.  Same kernels
+        # (knob) -> bit-identical; the default agrees to rounding.
+        dflt_f = so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan).data
+        plan.set_knob("dwt_seg", 1)
     ref_f = so3.fsoft_sequential(so3.So3SampleGrid(b, grid), plan).data
     ref_i = so3.ifsoft_sequential(so3.So3Coefficients(b, coeffs), plan).data
     plan.release()
     got_f, got_i = emulate(b, world, grid, coeffs, chunks)
     assert torch.equal(got_f, ref_f)
     assert torch.equal(got_i, ref_i)
-    del grid, got_f, got_i, ref_f, ref_i
+    if dflt_f is not None:
+        assert (dflt_f - ref_f).abs().max().item() <= 1e-14 * ref_f.abs().max().item()
+    del grid, got_f, got_i, ref_f, ref_i, dflt_f
     torch.cuda.empty_cache()
 
 
