@@ -75,16 +75,18 @@ __global__ void __launch_bounds__(128) dwt_checkpoint_kernel(DwtArgs a, double2*
 // last degree.  rows * SL entries, entry index i = row * SL + t.
 __device__ __forceinline__ void seg_stage_table(double2* lo, double2* hi, const double* rct, int rows, int SL, int SLP,
                                                 int nsteps, int t, int nt) {
-  for (int i = t; i < rows * SL; i += nt) {
-    const int rr = i / SL, tt = i - rr * SL;
-    double al = 0.0, cp = 0.0;
-    if (i < nsteps) {
-      al = __ldg(&rct[3 * i]);
-      cp = __ldg(&rct[3 * i + 1]);
+  const int lane = t & 31, nw = nt >> 5;
+  for (int rr = t >> 5; rr < rows; rr += nw)   // a table row per warp: no division per entry
+    for (int tt = lane; tt < SL; tt += 32) {
+      const int i = rr * SL + tt;
+      double al = 0.0, cp = 0.0;
+      if (i < nsteps) {
+        al = __ldg(&rct[3 * i]);
+        cp = __ldg(&rct[3 * i + 1]);
+      }
+      lo[rr * SLP + tt] = make_double2(al, cp);
+      hi[rr * SLP + tt] = make_double2(al, fma(-2.0, al, cp));
     }
-    lo[rr * SLP + tt] = make_double2(al, cp);
-    hi[rr * SLP + tt] = make_double2(al, fma(-2.0, al, cp));
-  }
 }
 
 constexpr int kSegTabA = kSegRows * (kSegMaxSL + 1);      // double2 per half, analysis (8 rows)
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_seg_kernel(DwtArgs
         const int l = m + i;
         double sc = (2.0 * l + 1.0) * rvscale * __ldg(&rct[3 * i + 2]);   // v_l * mu_l
         if ((M.sl * l + M.par0) & 1) sc = -sc;
-        a.coef[(long long)f * a.coef_fstride + coeff_slot(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
+        a.coef[(long long)f * a.coef_fstride + coeff_slot32(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
       }
     }
     // the next TB steps write the other buffer; this one is rewritten only after the next
@@ -213,7 +215,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_seg_kernel(DwtArgs
       }
       double sc = (2.0 * l + 1.0) * rvscale * __ldg(&rct[3 * i + 2]);
       if ((M.sl * l + M.par0) & 1) sc = -sc;
-      a.coef[(long long)f * a.coef_fstride + coeff_slot(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
+      a.coef[(long long)f * a.coef_fstride + coeff_slot32(l, M.pm, M.pmp)] = make_double2(re * sc, im * sc);
     }
   }
 }
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
             const int l = m + ii;
             double sc = (2.0 * l + 1.0) * rvscale * mus[ii];   // v_l * mu_l
             if (((o_neg[q] & 1) * l + (o_neg[q] >> 1)) & 1) sc = -sc;
-            a.coef[coeff_slot(l, (int)(o_pm[q] >> 32), (int)o_pm[q])] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
+            a.coef[coeff_slot32(l, (int)(o_pm[q] >> 32), (int)o_pm[q])] = make_double2((p0[q].x + re) * sc, (p0[q].y + im) * sc);
           }
         }
         // the next TB steps write the other buffer; this one is rewritten only after the next
@@ -540,36 +542,47 @@ __global__ void __launch_bounds__(WPC * 32, MINB) dwt_synthesis_seg_kernel(DwtAr
   // (the loads stay in flight: nothing here consumes them; the sign is applied when staging)
   // NT is a multiple of 8: a thread fetches the same member mm = t & 7 in every tile, so its
   // relation lives in registers and the first tiles go out with the recurrence state
-  static_assert(NT % 8 == 0, "member per thread");
+  static_assert(NT % 8 == 0 && TB % 2 == 0, "member per thread; the sign's parity is the same in every tile");
   const Member Mf = make_member(m, mp, t & 7, n);
-  auto fetch = [&](int t0, double2 (&pf)[PF], double (&pmu)[PF], unsigned& neg) {
-    neg = 0;
+  // Per-item constants of this thread (item q: member t & 7, step tb_q, segment kk_q of every tile):
+  // first degree index i0, live while t0 < lim, sign (-1)^(sl l + par0) (TB even: the same parity in
+  // every tile), destination in a staged tile.  The per-tile work is then a compare, a 32-bit slot
+  // (coeff_slot32), two loads; two multiplies and two stores when staging -- the 64-bit slot
+  // arithmetic and the index decoding per tile cost 1.7 ms of issue slots at B = 512.
+  int it_i0[PF], it_lim[PF], it_dst[PF];
+  bool it_neg[PF];
+#pragma unroll
+  for (int q = 0; q < PF; ++q) {
+    const int idx = t + q * NT;
+    const int mm = idx & 7, tb = (idx >> 3) % TB, kk = idx / (8 * TB);
+    it_i0[q] = kk * SL4 + tb;
+    it_lim[q] = (idx < 4 * TB * 8 && Mf.valid) ? min(SL4 - tb, nsteps - it_i0[q]) : 0;
+    it_neg[q] = ((Mf.sl * (m + it_i0[q]) + Mf.par0) & 1) != 0;
+    it_dst[q] = (kk * FR + tb * 8 + 2 * (mm & 3)) * 2 + (mm >> 2);   // in doubles
+  }
+  const double2* coef_f = a.coef + (long long)f * a.coef_fstride;
+  auto fetch = [&](int t0, double2 (&pf)[PF], double (&pmu)[PF]) {
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      const int idx = t + q * NT;
-      const int mm = idx & 7, tb = (idx >> 3) % TB, kk = idx / (8 * TB);
-      const int i = kk * SL4 + t0 + tb;
       double2 z = make_double2(0.0, 0.0);
       double mu = 0.0;
-      if (idx < 4 * TB * 8 && t0 + tb < SL4 && i < nsteps && Mf.valid) {
-        z = a.coef[(long long)f * a.coef_fstride + coeff_slot(m + i, Mf.pm, Mf.pmp)];
+      if (t0 < it_lim[q]) {
+        const int i = it_i0[q] + t0;
+        z = coef_f[coeff_slot32(m + i, Mf.pm, Mf.pmp)];
         mu = __ldg(&rct[3 * i + 2]);
-        if ((Mf.sl * (m + i) + Mf.par0) & 1) neg |= 1u << q;
       }
       pf[q] = z;
       pmu[q] = mu;
     }
   };
-  auto stage = [&](int bsel, const double2 (&pf)[PF], const double (&pmu)[PF], unsigned neg) {
+  auto stage = [&](int bsel, const double2 (&pf)[PF], const double (&pmu)[PF]) {
+    double* tile = reinterpret_cast<double*>(fco[bsel]);
 #pragma unroll
     for (int q = 0; q < PF; ++q) {
-      const int idx = t + q * NT;
-      if (idx < 4 * TB * 8) {
-        const int mm = idx & 7, tb = (idx >> 3) % TB, kk = idx / (8 * TB);
-        double* d = reinterpret_cast<double*>(&fco[bsel][kk * FR + tb * 8 + 2 * (mm & 3)]) + (mm >> 2);
-        const double mu = (neg >> q) & 1 ? -pmu[q] : pmu[q];
-        d[0] = pf[q].x * mu;
-        d[2] = pf[q].y * mu;
+      if (t + q * NT < 4 * TB * 8) {
+        const double mu = it_neg[q] ? -pmu[q] : pmu[q];
+        tile[it_dst[q]] = pf[q].x * mu;
+        tile[it_dst[q] + 2] = pf[q].y * mu;
       }
     }
   };
@@ -577,13 +590,12 @@ __global__ void __launch_bounds__(WPC * 32, MINB) dwt_synthesis_seg_kernel(DwtAr
   const double2* rw = rcs[2 * jw0 >= n ? 1 : 0] + k * SLP;
   double2 pf[PF], pf1[PF];
   double pmu[PF], pmu1[PF];
-  unsigned neg, neg1;
-  fetch(0, pf1, pmu1, neg1);
-  fetch(TB, pf, pmu, neg);   // tile 1 (zeros past the last step)
+  fetch(0, pf1, pmu1);
+  fetch(TB, pf, pmu);   // tile 1 (zeros past the last step)
   if (t < 8) mem[t] = member_of(a, m, mp, t);
   if (t == 0) seg_bar_init(&bar, NT);
   seg_stage_table(rcs[0], rcs[1], rct, 4, SL4, SLP, nsteps, t, NT);
-  stage(0, pf1, pmu1, neg1);
+  stage(0, pf1, pmu1);
   __syncthreads();
 
   // iteration i: stage tile i+1 (fetched during iteration i-1), arrive; fetch tile i+2; compute
@@ -595,9 +607,9 @@ __global__ void __launch_bounds__(WPC * 32, MINB) dwt_synthesis_seg_kernel(DwtAr
     const int bnext = bsel == 2 ? 0 : bsel + 1;
     const bool more = t0 + TB < SL4;
     if (more) {
-      stage(bnext, pf, pmu, neg);
+      stage(bnext, pf, pmu);
       seg_bar_arrive(&bar);
-      fetch(t0 + 2 * TB, pf, pmu, neg);
+      fetch(t0 + 2 * TB, pf, pmu);
     }
     const int nt = min(TB, SL4 - t0);
     const double2* fb = fco[bsel] + k * FR + r;
