@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
         const Member M = mem[4 * nt + tq];
         if (!M.valid) continue;
         const double sc = ((M.sl * l + M.par0) & 1) ? -vmu : vmu;
-        coef[coeff_slot(l, M.pm, M.pmp)] = make_double2(acc[mt][nt][0] * sc, acc[mt][nt][1] * sc);
+        coef[coeff_slot32(l, M.pm, M.pmp)] = make_double2(acc[mt][nt][0] * sc, acc[mt][nt][1] * sc);
       }
     }
   }
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int l = l0 + (lane >> 3) + 4 * i;
-      z[i] = (fvalid && Mk.valid && l < B) ? coef[coeff_slot(l, Mk.pm, Mk.pmp)] : make_double2(0.0, 0.0);
+      z[i] = (fvalid && Mk.valid && l < B) ? coef[coeff_slot32(l, Mk.pm, Mk.pmp)] : make_double2(0.0, 0.0);
     }
   };
   fetch(m);
