@@ -68,7 +68,9 @@ __device__ __forceinline__ Member make_member(int m, int mp, int k, int n) {
   r.par0 = (R.sm * m + R.smp * mp) & 1;
   r.pm = R.tm_m * m + R.tm_mp * mp;
   r.pmp = R.tp_m * m + R.tp_mp * mp;
-  const int bm = ((r.pm % n) + n) % n, bmp = ((r.pmp % n) + n) % n;
+  // |pm|, |pm'| < B = n / 2: the bin is the order itself or the order + n (no integer modulo: two
+  // runtime `%` cost ~80 instructions in every DWT prologue)
+  const int bm = r.pm < 0 ? r.pm + n : r.pm, bmp = r.pmp < 0 ? r.pmp + n : r.pmp;
   r.row = (long long)bmp * n + bm;
   return r;
 }

@@ -315,24 +315,31 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
 
   // round i of the snake: cluster i G + b (even i) or i G + G - 1 - b (odd i)
   auto cluster_of = [&](int i) { return i * G + ((i & 1) ? G - 1 - b : b); };
-  // warp 0: the operands of pass h of cluster c (base m, m') into the stage buffers, one bulk copy
-  // per lane (8 checkpoint rows, 8 member rows, v_j, the recurrence table)
-  auto prefetch = [&](int c, int h, int m, int mp, long long rco) {
-    const int j0 = h * WB;
+  // The operands of pass h of cluster c (base m, m') into the stage buffers: 18 bulk copies (8
+  // checkpoint rows, 8 member rows, v_j, the recurrence table), copy ci by lane 0 of warp ci mod W,
+  // so no warp falls behind the others by issuing them all (every batch barrier waits for the
+  // slowest warp).  Thread 0 registers the byte count first (prefetch_expect, before the barrier
+  // that frees the buffers); the copies follow it (prefetch_issue).
+  auto prefetch_expect = [&](int h, int m, int mp) {
     const int nsteps = B - m;
-    const Member M = make_member(m, mp, lane & 7, n);
-    const unsigned nvalid = __popc(__ballot_sync(0xffffffffu, M.valid && lane < 8));
+    const int nvalid = m == 0 ? 1 : (mp == 0 || mp == m) ? 4 : 8;
     const unsigned tabb = h == 0 ? (unsigned)(((nsteps + 1) & ~1) * 24) : 0u;
-    if (lane == 0) seg_expect_tx(&bar, (unsigned)((kSegRows + nvalid) * WB * 16 + WB * 8) + tabb);
-    __syncwarp();
-    if (lane < 8) {
-      seg_bulk_load(ckS + lane * RS, ck + ((long long)c * kSegRows + lane) * n + j0, WB * 16, &bar);
-    } else if (lane < 16) {
-      if (M.valid) seg_bulk_load(xS + (lane - 8) * RS, a.spec + M.row * n + (M.reflect ? n - j0 - WB : j0), WB * 16, &bar);
-    } else if (lane == 16) {
-      seg_bulk_load(vS, a.xv + j0, WB * 8, &bar);
-    } else if (lane == 17 && h == 0) {
-      seg_bulk_load(rcS, a.rc + 3 * rco, tabb, &bar);
+    seg_expect_tx(&bar, (unsigned)((kSegRows + nvalid) * WB * 16 + WB * 8) + tabb);
+  };
+  auto prefetch_issue = [&](int c, int h, int m, int mp, long long rco) {
+    if (lane != 0) return;
+    const int j0 = h * WB;
+    for (int ci = warp; ci < 18; ci += W) {
+      if (ci < 8) {
+        seg_bulk_load(ckS + ci * RS, ck + ((long long)c * kSegRows + ci) * n + j0, WB * 16, &bar);
+      } else if (ci < 16) {
+        const Member M = make_member(m, mp, ci - 8, n);
+        if (M.valid) seg_bulk_load(xS + (ci - 8) * RS, a.spec + M.row * n + (M.reflect ? n - j0 - WB : j0), WB * 16, &bar);
+      } else if (ci == 16) {
+        seg_bulk_load(vS, a.xv + j0, WB * 8, &bar);
+      } else if (h == 0) {
+        seg_bulk_load(rcS, a.rc + 3 * rco, (unsigned)(((B - m + 1) & ~1) * 24), &bar);
+      }
     }
   };
 
@@ -346,7 +353,9 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
   // (m, m', table offset) of the current cluster and of the next one, loaded a pass ahead
   int2 base = __ldg(&a.bases[a.cluster0 + c0]);
   long long rco = __ldg(&a.rc_off[a.cluster0 + c0]);
-  if (warp == 0) prefetch(a.cluster0 + c0, 0, base.x, base.y, rco);
+  if (t == 0) prefetch_expect(0, base.x, base.y);
+  __syncthreads();
+  prefetch_issue(a.cluster0 + c0, 0, base.x, base.y, rco);
   unsigned parity = 0;
   for (int i = 0;; ++i) {
     const int c = a.cluster0 + cluster_of(i);
@@ -364,7 +373,11 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
       parity ^= 1;
       const int j0 = h * WB;
       // padded table rows and mu_l from the raw table (which stays until the next cluster's pass 0 arrives)
-      if (h == 0 && t < 8) mem[t] = make_member(m, mp, t, n);
+      if (h == 0 && lane == 0 && warp < 8) {   // a member per warp (W < 8: the remaining ones by warp 0)
+        mem[warp] = make_member(m, mp, warp, n);
+        if (warp == 0)
+          for (int mmx = W; mmx < 8; ++mmx) mem[mmx] = make_member(m, mp, mmx, n);
+      }
       const bool both = halves == 1;         // the CTA spans [0, pi): both table halves
       const bool upper_pass = 2 * j0 >= n;   // halves > 1: the pass lies in one half
       for (int rr = warp; rr < kSegRows; rr += W) {   // one table row per warp: no division per entry
@@ -404,11 +417,13 @@ __global__ void __launch_bounds__(WT * 32, MINB) dwt_analysis_segp_kernel(DwtArg
           xi[g] = z.y;
         }
       }
-      __syncthreads();   // the stage buffers are free; the padded table, mu and the members are visible
-      if (warp == 0) {   // next pass: the other half of this cluster, or the next cluster
-        if (h + 1 < halves) prefetch(c, h + 1, m, mp, rco);
-        else if (cn < ncl) prefetch(a.cluster0 + cn, 0, base_n.x, base_n.y, rco_n);
+      if (t == 0) {   // the next pass's byte count: the other half of this cluster, or the next cluster
+        if (h + 1 < halves) prefetch_expect(h + 1, m, mp);
+        else if (cn < ncl) prefetch_expect(0, base_n.x, base_n.y);
       }
+      __syncthreads();   // the stage buffers are free; the padded table, mu and the members are visible
+      if (h + 1 < halves) prefetch_issue(c, h + 1, m, mp, rco);
+      else if (cn < ncl) prefetch_issue(a.cluster0 + cn, 0, base_n.x, base_n.y, rco_n);
       const double2* rw = rcs + ((both && 2 * (j0 + jl0) >= n) ? kSegRows * SLP : 0) + r * SLP;
       const bool last = h + 1 == halves;
       // Per-pass constants of this thread's outputs: output q is entry o_q of step tb_q of every batch
