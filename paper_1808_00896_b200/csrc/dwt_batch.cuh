@@ -64,8 +64,18 @@ __host__ __device__ inline size_t batch_synthesis_smem(int n) {
 // (lane (g, tq) reads member (g/2)'s re or im part at beta 4s + tq, mirrored for reflecting
 // members: every fetched sector is used).  No staging buffer, so the CTA holds only the
 // shared Wigner tile and FC = 4 functions give 4 independent CTAs per SM.
+// Seeds d^m_{m,m'}(beta_j) of every (cluster, beta index), once per plan: every CTA of a cluster (one per
+// function group) otherwise repeats the double-double log-space evaluation and its exp() in its
+// prologue (same function and inputs: the table holds the identical bits).
+__global__ void __launch_bounds__(64) dwt_seed_table_kernel(DwtArgs a, double* seeds) {
+  const int c = blockIdx.x, j = threadIdx.x + 64 * blockIdx.y;
+  if (j >= a.n) return;
+  const int2 base = __ldg(&a.bases[c]);
+  seeds[(long long)c * a.n + j] = seed_value(base.x, base.y, __ldg(&a.lnorm[c]), a.logcs[j]);
+}
+
 template <int FC, int KSM>
-__global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtArgs a, int batch) {
+__global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtArgs a, int batch, const double* seeds) {
   extern __shared__ double dsm[];
   __shared__ Member mem[8];
   const int c = a.cluster0 + blockIdx.x;
@@ -78,7 +88,6 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
   const int fl = warp;
   const bool fvalid = f0 + fl < batch;
   const long long rco = __ldg(&a.rc_off[c]);
-  const double2 ln = __ldg(&a.lnorm[c]);
   double* D = dsm;                                   // [32][sd]
   if (t < 8) mem[t] = member_of(a, m, mp, t);
   __syncthreads();
@@ -102,7 +111,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
   double x = 0.0, cur = 0.0, prev = 0.0;
   if (t < n) {
     x = __ldg(&a.xv[t]);
-    cur = seed_value(m, mp, ln, a.logcs[t]);
+    cur = __ldg(&seeds[(long long)c * n + t]);
   }
   const bool two_tiles = mem[4].valid;
   const double vscale = 8.0 * 3.141592653589793 * (double)B;
@@ -153,7 +162,7 @@ __global__ void __launch_bounds__(FC * 32, 4) dwt_analysis_batch_reg_kernel(DwtA
 // Warp w stages the signed coefficients of function f0 + w (8 per lane per 32-degree tile,
 // fetched one tile ahead) and owns its output; only the Wigner tile is shared.
 template <int FC, int MTMAX>
-__global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs a, int batch) {
+__global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs a, int batch, const double* seeds) {
   constexpr int SF = FC * 16 + 4;
   extern __shared__ double dsm[];
   __shared__ Member mem[8];
@@ -188,7 +197,7 @@ __global__ void __launch_bounds__(FC * 32, 2) dwt_synthesis_batch_kernel(DwtArgs
   double x = 0.0, cur = 0.0, prev = 0.0;
   if (t < n) {
     x = __ldg(&a.xv[t]);
-    cur = seed_value(m, mp, __ldg(&a.lnorm[c]), a.logcs[t]);
+    cur = __ldg(&seeds[(long long)c * n + t]);
   }
   const bool two_tiles = mem[4].valid;
   const int mtn = np >> 3;

@@ -212,6 +212,7 @@ struct so3_plan_s {
   int dwt_seg = 1;                // knob, bits: 1 = segment-parallel synthesis, 2 = analysis, 4 = persistent analysis (B % 64 == 0)
   int seg_ana_w = 8;              // knob: most warps per analysis CTA (8: one CTA per SM; 4: two)
   double2* d_ck = nullptr;
+  double* d_seed = nullptr;       // batched plans with 2B <= 64: recurrence seeds per (cluster, beta index)
   int pbuf_splits = 0;            // partial sets d_pbuf holds
   int fft_wide = 0;   // dev knob (SO3_FFT_XB): rows per FFT CTA override
   int fft_fused = 1;  // 2B <= 64: one-pass 2-D slice transform (fft2d_slice_kernel)
@@ -630,24 +631,25 @@ int launch_dwt_syn_wpc(const so3::DwtArgs& a, int split, unsigned ncl, int batch
 
 
 template <int JW, int FG = 1>
-int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+int launch_dwt_mma_cta(const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st, const double2* ck = nullptr) {
   using SM = so3::MmaSmem<JW>;
   const int warps = (n + JW - 1) / JW;
   const size_t smem = ((size_t)warps * 8 * SM::S + 2 * (size_t)warps * 512 * FG) * sizeof(double);
   auto k = straddles(a, JW) ? so3::dwt_analysis_mma_cta_kernel<JW, FG, 8, 1, true>
                             : so3::dwt_analysis_mma_cta_kernel<JW, FG, 8, 1, false>;
   SO3_CUDA(set_smem(k, smem));
-  k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a, so3::SplitArgs{nullptr, 0, nullptr});
+  k<<<dim3(ncl, batch / FG), warps * 32, smem, st>>>(a, so3::SplitArgs{nullptr, 0, nullptr, ck});
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
 }
 
 template <int JW>
-int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st,
+                   const double2* ck = nullptr) {
   const int warps = (n + JW - 1) / JW;
   if (analysis) {
     if (warps > 8) return fail(SO3_ERR_INVALID, "bandwidth too large for the MMA DWT kernels");
-    return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st);
+    return launch_dwt_mma_cta<JW>(a, n, ncl, batch, st, ck);
   }
   if constexpr (JW == 32) {
     if (batch % 4 == 0) {   // batched small B: 4 functions share each recurrence
@@ -663,17 +665,18 @@ int launch_dwt_mma(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, in
 
 // Batched plans with 2B <= 64: analysis 4 functions per CTA (register operands), synthesis
 // 8 functions per CTA (staged coefficients), see dwt_batch.cuh.
-int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, cudaStream_t st) {
+int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, int batch, const double* seeds,
+                     cudaStream_t st) {
   if (analysis) {
     constexpr int FC = 4;
     auto k = so3::dwt_analysis_batch_reg_kernel<FC, 16>;
-    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, so3::batch_analysis_smem(n), st>>>(a, batch);
+    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, so3::batch_analysis_smem(n), st>>>(a, batch, seeds);
   } else {
     constexpr int FC = 8;
     const size_t smem = so3::batch_synthesis_smem<FC>(n);
     auto k = so3::dwt_synthesis_batch_kernel<FC, 8>;
     SO3_CUDA(set_smem(k, smem));
-    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, smem, st>>>(a, batch);
+    k<<<dim3(ncl, (batch + FC - 1) / FC), FC * 32, smem, st>>>(a, batch, seeds);
   }
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -684,7 +687,7 @@ int launch_dwt_batch(bool analysis, const so3::DwtArgs& a, int n, unsigned ncl, 
 // ana_split knob turns the split on, never on the launch path (graph capture, stream order).
 int launch_dwt_ana_split(const so3_plan_s* p, so3::DwtArgs a, unsigned ncl, cudaStream_t st) {
   if (!p->d_pbuf || !p->d_pcnt) return fail(SO3_ERR_INVALID, "split analysis without its plan scratch");
-  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt, p->d_ck};
   constexpr int JW = 128;
   const int W = p->n / JW / 2;   // warps per half
   using SM = so3::MmaSmem<JW>;
@@ -716,7 +719,7 @@ int launch_seg_ana_cfg(const so3_plan_s* p, const so3::DwtArgs& a, unsigned ncl,
   auto k = so3::dwt_analysis_seg_kernel<16, SPLIT, TB, MINB, WT>;
   const size_t smem = ((size_t)2 * so3::kSegTabA + (size_t)2 * TB * W * 64) * sizeof(double2) + (size_t)t_knobs.dwt_pad * 1024;
   SO3_CUDA(set_smem(k, smem));
-  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt, p->d_ck};
   k<<<dim3(ncl * SPLIT, SPLIT > 1 ? 1 : p->batch), W * 32, smem, st>>>(a, sp, p->d_ck);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -759,7 +762,7 @@ int launch_seg_ana_persist(const so3_plan_s* p, const so3::DwtArgs& a, unsigned 
     }
     grid = it->second;
   }
-  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt};
+  const so3::SplitArgs sp{p->d_pbuf, p->rc_entries * 8, p->d_pcnt, p->d_ck};
   k<<<std::min<unsigned>(ncl, (unsigned)grid), W * 32, smem, st>>>(a, sp, p->d_ck, (int)ncl, halves);
   SO3_CUDA(cudaGetLastError());
   return SO3_OK;
@@ -814,8 +817,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
   // sharded: spec is one chunk [h][pairs_chunk][J] of layout B (chunk_pairs; default = all pairs)
   a.slab_stride = p->sharded ? (long long)(chunk_pairs >= 0 ? chunk_pairs : p->pairs_rank) * p->J : 0;
   const unsigned ncl = (unsigned)(c1 - c0);
-  if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64)
-    return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, st);
+  if (p->dwt_variant != SO3_DWT_SIMT && p->dwt_batch && p->batch >= 2 && p->n <= 64 && p->d_seed)
+    return launch_dwt_batch(ANALYSIS, a, p->n, ncl, p->batch, p->d_seed, st);
   if (ANALYSIS && seg_applies(p) && (p->dwt_seg & 4) && !p->sharded && p->batch == 1 && p->n / so3::kSegBeta >= 4)
     return launch_dwt_seg_anap(p, a, ncl, st);
   if (seg_applies(p) && (p->dwt_seg & (ANALYSIS ? 2 : 1)) && (!ANALYSIS || seg_ana_split(p) == 1 || p->batch == 1))
@@ -830,8 +833,8 @@ int launch_dwt(const so3_plan_s* p, const void* spec, void* coef, int64_t c0, in
     return launch_dwt_ana_split(p, a, ncl, st);
   if (p->dwt_variant != SO3_DWT_SIMT && (p->n + dwt_jw(p->n) - 1) / dwt_jw(p->n) <= 8) {
     switch (dwt_jw(p->n)) {
-      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st);
-      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st);
+      case 128: return launch_dwt_mma<128>(ANALYSIS, a, p->n, ncl, p->batch, st, p->d_ck);
+      case 64: return launch_dwt_mma<64>(ANALYSIS, a, p->n, ncl, p->batch, st, p->d_ck);
       default: return launch_dwt_mma<32>(ANALYSIS, a, p->n, ncl, p->batch, st);
     }
   }
@@ -1126,6 +1129,21 @@ int build_plan(so3_plan_s* p, const std::vector<Cluster>& cl) {
   }
   e = e ? e : cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+  if (p->batch >= 2 && n <= 64 && !cl.empty()) {   // seed table of the batched kernels (dwt_batch.cuh)
+    const size_t bytes = cl.size() * n * sizeof(double);
+    if (cudaMalloc((void**)&p->d_seed, bytes) != cudaSuccess) return fail(SO3_ERR_NOMEM, "seed table");
+    so3::DwtArgs sa{};
+    sa.B = b;
+    sa.n = n;
+    sa.bases = p->d_bases;
+    sa.lnorm = p->d_lnorm;
+    sa.logcs = p->d_logcs;
+    so3::dwt_seed_table_kernel<<<dim3((unsigned)cl.size(), (n + 63) / 64), 64>>>(sa, p->d_seed);
+    cudaError_t se = cudaGetLastError();
+    se = se ? se : cudaDeviceSynchronize();
+    if (se != cudaSuccess) return fail(SO3_ERR_CUDA, std::string("seed table: ") + cudaGetErrorString(se));
+    p->bytes += (int64_t)bytes;
+  }
   if (int rc = ensure_checkpoints(p)) return rc;
   if (split_applies(p)) return ensure_split_scratch(p);
   return SO3_OK;
@@ -1316,6 +1334,7 @@ void so3_plan_destroy(so3_plan_t p) {
   cudaFree(p->d_pbuf);
   cudaFree(p->d_pcnt);
   cudaFree(p->d_ck);
+  cudaFree(p->d_seed);
   cudaFree(p->d_row_global);
   cudaFree(p->d_row_local);
   cudaFree(p->d_grid_stage);
