@@ -168,7 +168,9 @@ int so3_plan_set_dwt_variant(so3_plan_t plan, int variant);
  * with one CTA per cluster part, 4 = persistent analysis with bulk-copy operand prefetch on
  * single-device one-function plans; 0 = dwt_mma.cuh kernels; same results to rounding,
  * deterministic; default 1, and 1 | 4 at B = 320 .. 512, where the persistent analysis is 6-9 %
- * faster than dwt_analysis_mma_cta_kernel; at B <= 256 that kernel is as fast and stays), "seg_ana_w" (warps per CTA of those analysis variants, 4 or 8).
+ * faster than dwt_analysis_mma_cta_kernel; at B <= 256 that kernel is as fast and stays; the
+ * persistent kernel keeps one CTA with ~222 KB of shared memory on every SM for its duration, so
+ * kernels of other streams do not run beside it), "seg_ana_w" (warps per CTA of those analysis variants, 4 or 8).
  * Experiment knobs (same results,
  * measured slower or equal): "fft_persist" (> 0: the
  * TMA passes as that many persistent double-buffered CTAs), "fft_pad" / "dwt_pad" (extra KB of
